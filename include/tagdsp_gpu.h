@@ -1,0 +1,148 @@
+/* tagdsp_gpu.h -- C-ABI of the B200-native acquisition (searching) hot path.
+ *
+ * Drop-in replacement for the reference tagdsp detector path
+ * (/root/reference/proj): sample block in, per-tag detections out.  The
+ * reference has no FFI layer (a C++20 static library, proj/src/CMakeLists.txt:1-12);
+ * each entry point below names the reference function it replaces, and the
+ * header-only C++ wrapper include/tagdsp_gpu.hpp restores the reference
+ * signatures on top of it.  Plain pointers and sizes only; no torch or CUDA
+ * types.  Every call returns TDG_OK (0) or an error code from
+ * tagdsp_gpu_types.h, with a message in tdg_last_error().
+ *
+ * Objects (all device-resident, "allocate once, reuse" like PlanCache,
+ * proj/include/tagdsp/fft.hpp:13-16):
+ *   tdg_ctx      one CUDA device + stream + FFT plans/tables (~ PlanCache)
+ *   tdg_codeset  prepared codes for one window shape (~ CodeCache entries,
+ *                proj/include/tagdsp/detector.hpp:26-37)
+ *   tdg_windows  demodulated windows d,u for W samples x (windows x bins)
+ *                (~ DemodResult, proj/include/tagdsp/dsp.hpp:62-65)
+ */
+#ifndef TAGDSP_GPU_H
+#define TAGDSP_GPU_H
+#include <stddef.h>
+#include <stdint.h>
+
+#include "tagdsp_gpu_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tdg_ctx tdg_ctx;
+typedef struct tdg_codeset tdg_codeset;
+typedef struct tdg_windows tdg_windows;
+
+/* Message for the last failing call on this host thread. */
+const char* tdg_last_error(void);
+/* Library version string and number of CUDA kernels launched by this
+ * process (all contexts) -- used by bench.py's gpu_launches accounting. */
+const char* tdg_version(void);
+uint64_t tdg_kernel_launches(void);
+
+/* PlanCache construction (proj/src/fft.cpp:27-44 creates plans lazily; here
+ * the context owns the stream and the twiddle tables of every supported
+ * transform length). */
+int tdg_ctx_create(int device, tdg_ctx** out);
+void tdg_ctx_destroy(tdg_ctx* ctx);
+int tdg_ctx_synchronize(tdg_ctx* ctx);
+/* Raw cudaStream_t of the context (opaque pointer), for event timing. */
+void* tdg_ctx_stream(tdg_ctx* ctx);
+
+/* pad_length (proj/src/fft.cpp:93-101): smallest {2,3,5,7}-smooth m >= n. */
+uint64_t tdg_pad_length(uint64_t n);
+/* Transform length the B200 path uses for a correlation that must be linear
+ * over lags [0, window_len) for supports up to nonzero_len: the smallest
+ * supported N1*N2 >= window_len + nonzero_len - 1 (0 if unsupported).  Any
+ * such length gives the same lags as the reference's corr_len
+ * (proj/include/tagdsp/detector.hpp:19-21); only rounding differs. */
+uint64_t tdg_corr_len(uint64_t window_len, uint64_t nonzero_len);
+
+/* ---- codes ---------------------------------------------------------------
+ * prepare_code (proj/src/detector.cpp:50-66) for n_codes codes at once, all
+ * on the GPU: synth_replica (proj/src/codegen.cpp:40-60) -> demodulation
+ * with lo_freq = 0 (proj/src/dsp.cpp:159-191) -> support / energy / abs_sum
+ * (proj/src/detector.cpp:20-43) -> forward FFT of the zero-padded replica d
+ * (:45-47).  bits is n_codes x cfg->mod.packet_bits bytes (0/1).
+ * Errors as the reference: window_len < packet_samples -> TDG_EINVAL. */
+int tdg_codeset_prepare(tdg_ctx* ctx, const tdg_demod_config* cfg, uint64_t window_len,
+                        const uint8_t* bits, uint64_t n_codes, tdg_codeset** out);
+/* make_transformed (proj/src/detector.cpp:11-48) from host replicas:
+ * replica_d/replica_u are n_codes pointers to `lengths[i]` floats
+ * (replica_u may be NULL -> support measured on d).  corr_len is the
+ * reference's transform length and is only used for its precondition
+ * (window_len + n <= corr_len + 1, else TDG_EINVAL). */
+int tdg_codeset_from_replicas(tdg_ctx* ctx, uint64_t window_len, uint64_t corr_len,
+                              const float* const* replica_d, const float* const* replica_u,
+                              const uint64_t* lengths, uint64_t n_codes, tdg_codeset** out);
+void tdg_codeset_destroy(tdg_codeset* cs);
+uint64_t tdg_codeset_size(const tdg_codeset* cs);
+/* TransformedCode fields (proj/include/tagdsp/detector.hpp:26-35). */
+int tdg_codeset_info(const tdg_codeset* cs, uint64_t idx, uint64_t* nonzero_len, float* energy,
+                     float* abs_sum, uint64_t* corr_len);
+int tdg_codeset_replica(const tdg_codeset* cs, uint64_t idx, float* replica_d_out);
+
+/* ---- windows -------------------------------------------------------------
+ * Storage for n_windows x n_bins demodulated windows of window_len samples. */
+int tdg_windows_create(tdg_ctx* ctx, uint64_t window_len, uint64_t n_windows, uint64_t n_bins,
+                       tdg_windows** out);
+void tdg_windows_destroy(tdg_windows* w);
+/* demodulate_window (proj/src/dsp.cpp:193-197) for every window w < n_windows
+ * starting at stream sample w*advance of `iq` (interleaved int16 I,Q, HOST
+ * memory, n_complex samples, absolute start index stream_start) and every
+ * lo_freq in lo_bins (the frequency-offset sweep; the reference's single
+ * DemodConfig::lo_freq is lo_bins[0] with n_bins = 1).  Slot of (w, b) is
+ * w*n_bins + b.  cfg->lo_freq is ignored (the bins replace it). */
+int tdg_demodulate(tdg_ctx* ctx, tdg_windows* win, const tdg_demod_config* cfg,
+                   const double* lo_bins, uint64_t n_bins, const int16_t* iq, uint64_t n_complex,
+                   int64_t stream_start, uint64_t advance, uint64_t n_windows);
+/* Same as tdg_demodulate but `iq_dev` is a device pointer (already resident). */
+int tdg_demodulate_device(tdg_ctx* ctx, tdg_windows* win, const tdg_demod_config* cfg,
+                          const double* lo_bins, uint64_t n_bins, const int16_t* iq_dev,
+                          uint64_t n_complex, int64_t stream_start, uint64_t advance,
+                          uint64_t n_windows);
+/* detect(d, u, ...) entry: upload a host d,u pair into a slot. */
+int tdg_windows_set_du(tdg_ctx* ctx, tdg_windows* w, uint64_t slot, const float* d, const float* u,
+                       int64_t window_start);
+int tdg_windows_get_du(tdg_ctx* ctx, const tdg_windows* w, uint64_t slot, float* d, float* u);
+
+/* ---- detection -----------------------------------------------------------
+ * detect (proj/src/detector.cpp:167-206) for every slot x code: one forward
+ * FFT per slot, then per (slot, code) the fused spectral product + inverse
+ * FFT + |xc| first-index argmax (the xc vector never reaches HBM), then
+ * parabolic refinement, (w_c, q, p_c) statistics, score, ToA and accept.
+ * out receives n_slots*n_codes records ordered [slot][code] (slot = window *
+ * n_bins + bin) in HOST memory.  toa uses each slot's window_start. */
+int tdg_detect(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float threshold,
+               double sample_rate, tdg_detection* out);
+/* batch_xcorr (proj/src/detector.cpp:102-120) for one slot: the full xc
+ * (lags [0, W)) of each requested code, normalised like the reference
+ * inverse (1/N), into HOST out (n_idx x W).  Test/diagnostic path. */
+int tdg_batch_xcorr(tdg_ctx* ctx, tdg_windows* w, uint64_t slot, const tdg_codeset* cs,
+                    const int64_t* idx, uint64_t n_idx, float* out);
+
+/* ---- whole searching pass ------------------------------------------------
+ * detect_recording (proj/src/recording.cpp:258-289) with a frequency-offset
+ * sweep: windows of window_len every `advance` samples over a HOST int16
+ * stream, every code x every bin.  H2D of the stream, demodulation, all
+ * correlations, statistics and the D2H of the detections happen inside.
+ * out must hold n_windows*n_bins*n_codes records, n_windows =
+ * (n_complex >= window_len) ? (n_complex - window_len)/advance + 1 : 0. */
+int tdg_search(tdg_ctx* ctx, const tdg_demod_config* cfg, const double* lo_bins, uint64_t n_bins,
+               const int16_t* iq, uint64_t n_complex, int64_t stream_start, uint64_t window_len,
+               uint64_t advance, const tdg_codeset* cs, float threshold, tdg_detection* out,
+               uint64_t out_cap, uint64_t* n_out);
+
+/* Tuning / profiling knobs (0 = default): "wave_pairs", "fwd_wave",
+ * "time_kernels" (1 = record a CUDA event pair on the context stream around
+ * every launch; read back with tdg_kernel_time). */
+int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value);
+/* Launch count and summed device time (ms) of one kernel family since the
+ * last reset: "demod", "fwd_pass1", "fwd_pass2", "corr_passA", "corr_passB",
+ * "stats".  Synchronises the context stream. */
+int tdg_kernel_time(tdg_ctx* ctx, const char* name, uint64_t* count, double* total_ms);
+int tdg_kernel_time_reset(tdg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

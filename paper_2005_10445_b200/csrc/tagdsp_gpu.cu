@@ -1,0 +1,1152 @@
+// Host side of the B200 acquisition path: contexts, transform plans, code
+// sets, window sets, launch orchestration and the extern "C" ABI declared in
+// include/tagdsp_gpu.h.  Kernels live in kernels.cuh.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <complex>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tagdsp_gpu.h"
+#include "kernels.cuh"
+#include "corr_v2.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    throw Error(code, buf);
+}
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(e == cudaErrorMemoryAllocation ? TDG_ENOMEM : TDG_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(x) ck((x), #x)
+#define LAUNCHED()                                              \
+    do {                                                        \
+        g_launches.fetch_add(1, std::memory_order_relaxed);     \
+        ck(cudaGetLastError(), "kernel launch");                \
+    } while (0)
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return TDG_OK;
+    } catch (const Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return TDG_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return TDG_EINTERNAL;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Device buffer
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        release();
+        CK(cudaMalloc(&p, b));
+        bytes = b;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+// Descriptor staging: one pinned host buffer + one device buffer per pack,
+// uploaded with a single async copy; the next reuse waits on the copy's event.
+struct DescPack {
+    char* host = nullptr;
+    size_t cap = 0, used = 0;
+    DevBuf dev;
+    cudaEvent_t done = nullptr;
+    bool pending = false;
+    DescPack() = default;
+    DescPack(const DescPack&) = delete;
+    DescPack& operator=(const DescPack&) = delete;
+    ~DescPack() {
+        if (done) cudaEventDestroy(done);
+        if (host) cudaFreeHost(host);
+    }
+    void begin() {
+        if (pending) CK(cudaEventSynchronize(done));
+        pending = false;
+        used = 0;
+    }
+    template <class T>
+    size_t add(const std::vector<T>& v) {
+        const size_t off = (used + 255) & ~size_t(255);
+        const size_t need = off + v.size() * sizeof(T);
+        if (need > cap) {
+            size_t ncap = std::max(need, cap * 2 + 4096);
+            char* nh = nullptr;
+            CK(cudaHostAlloc(reinterpret_cast<void**>(&nh), ncap, cudaHostAllocDefault));
+            if (host) {
+                std::memcpy(nh, host, used);
+                cudaFreeHost(host);
+            }
+            host = nh;
+            cap = ncap;
+        }
+        if (!v.empty()) std::memcpy(host + off, v.data(), v.size() * sizeof(T));
+        used = need;
+        return off;
+    }
+    void commit(cudaStream_t st) {
+        if (!done) CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        dev.ensure(std::max<size_t>(used, 256));
+        if (used) CK(cudaMemcpyAsync(dev.p, host, used, cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(done, st));
+        pending = true;
+    }
+    template <class T>
+    T* at(size_t off) const { return reinterpret_cast<T*>(static_cast<char*>(dev.p) + off); }
+};
+
+// ---------------------------------------------------------------------------
+// Supported pass lengths L = P*Q (register codelets P and Q, tools/gen_codelets.py).
+#define TDG_MENU(X) \
+    X(16, 4, 4)     \
+    X(32, 4, 8)     \
+    X(64, 8, 8)     \
+    X(128, 8, 16)   \
+    X(256, 16, 16)  \
+    X(360, 18, 20)  \
+    X(450, 18, 25)  \
+    X(512, 16, 32)  \
+    X(864, 27, 32)  \
+    X(1008, 28, 36) \
+    X(1024, 32, 32)
+
+struct PassShape {
+    int L, P, Q;
+};
+const PassShape kMenu[] = {
+#define X(L, P, Q) {L, P, Q},
+    TDG_MENU(X)
+#undef X
+};
+constexpr int kMenuN = sizeof(kMenu) / sizeof(kMenu[0]);
+
+const PassShape& shape_of(int L) {
+    for (const auto& s : kMenu)
+        if (s.L == L) return s;
+    fail(TDG_ERANGE, "unsupported pass length %d", L);
+}
+
+constexpr int kTB = 8;   // t2 columns per CTA in the chunked passes (F1, B)
+constexpr int kG = 2;    // code pairs per pass-A work item
+constexpr int kDemodBlk = 4;
+
+uint64_t pad_length_impl(uint64_t n) {
+    if (n < 1) fail(TDG_EINVAL, "pad_length: n must be >= 1");
+    for (uint64_t m = n;; ++m) {
+        uint64_t r = m;
+        for (uint64_t p : {2, 3, 5, 7})
+            while (r % p == 0) r /= p;
+        if (r == 1) return m;
+    }
+}
+
+// smallest N1*N2 >= need; ties -> more balanced split (pass B is the chunked one)
+bool choose_corr_len(uint64_t need, int* n1, int* n2) {
+    uint64_t best = 0;
+    int b1 = 0, b2 = 0;
+    for (const auto& a : kMenu)
+        for (const auto& b : kMenu) {
+            const uint64_t n = uint64_t(a.L) * uint64_t(b.L);
+            if (n < need) continue;
+            const bool better = best == 0 || n < best ||
+                                (n == best && std::abs(a.L - b.L) < std::abs(b1 - b2)) ||
+                                (n == best && std::abs(a.L - b.L) == std::abs(b1 - b2) && a.L > b1);
+            if (better) {
+                best = n;
+                b1 = a.L;
+                b2 = b.L;
+            }
+        }
+    if (!best) return false;
+    *n1 = b1;
+    *n2 = b2;
+    return true;
+}
+
+// ---------------------------------------------------------------------------
+// Kernel dispatch by pass length
+template <class T>
+void set_smem(T* kernel, size_t bytes) {
+    if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+}
+
+int block_for(int tasks) {
+    int t = ((tasks + 31) / 32) * 32;
+    return std::min(256, std::max(32, t));
+}
+
+void launch_fwd1(int L, dim3 grid, cudaStream_t st, const tdg::SeqPairDesc* pairs, int N2, const float2* tw) {
+    switch (L) {
+#define X(LL, P, Q)                                                                        \
+    case LL: {                                                                             \
+        const size_t sm = size_t(P) * Q * kTB * sizeof(float2);                            \
+        set_smem(tdg::k_fwd_pass1<P, Q, kTB>, sm);                                         \
+        tdg::k_fwd_pass1<P, Q, kTB><<<grid, block_for(std::max(P, Q) * kTB), sm, st>>>(pairs, N2, tw); \
+        LAUNCHED();                                                                        \
+        return;                                                                            \
+    }
+        TDG_MENU(X)
+#undef X
+    }
+    fail(TDG_ERANGE, "fwd1: length %d", L);
+}
+
+void launch_fwd2(int L, bool split, dim3 grid, cudaStream_t st, const tdg::SeqPairDesc* pairs, int N1,
+                 const float2* tw) {
+    switch (L) {
+#define X(LL, P, Q)                                                                                       \
+    case LL: {                                                                                            \
+        constexpr int QS = (Q % 2) ? Q : Q + 1;                                                           \
+        const size_t sm = (size_t(2) * P * QS + 2 * LL + 2 * (P + Q)) * sizeof(float2);                   \
+        if (split) {                                                                                      \
+            set_smem(tdg::k_fwd_pass2<P, Q, true>, sm);                                                   \
+            tdg::k_fwd_pass2<P, Q, true><<<grid, block_for(2 * std::max(P, Q)), sm, st>>>(pairs, N1, tw);  \
+        } else {                                                                                          \
+            set_smem(tdg::k_fwd_pass2<P, Q, false>, sm);                                                  \
+            tdg::k_fwd_pass2<P, Q, false><<<grid, block_for(2 * std::max(P, Q)), sm, st>>>(pairs, N1, tw); \
+        }                                                                                                 \
+        LAUNCHED();                                                                                       \
+        return;                                                                                           \
+    }
+        TDG_MENU(X)
+#undef X
+    }
+    fail(TDG_ERANGE, "fwd2: length %d", L);
+}
+
+int g_num_sms = 0;
+
+int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return g_num_sms;
+}
+
+template <class K>
+int persistent_grid(K* kernel, int threads, size_t smem, int n_items) {
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+    if (per_sm < 1) fail(TDG_ECUDA, "kernel does not fit on an SM (smem %zu)", smem);
+    return std::max(1, std::min(n_items, per_sm * num_sms()));
+}
+
+void launch_corrA(int L, cudaStream_t st, const tdg::CorrGroup<kG>* groups, int n_groups, int N1, const float2* tw) {
+    const int n_items = (N1 / 2 + 1) * n_groups;
+    switch (L) {
+#define X(LL, P, Q)                                                                                 \
+    case LL: {                                                                                      \
+        using C = tdg::PassA2<P, Q, kG>;                                                            \
+        auto* k = tdg::k_corr_passA2<P, Q, kG>;                                                     \
+        const int grid = persistent_grid(k, C::NT, C::SMEM, n_items);                               \
+        k<<<grid, C::NT, C::SMEM, st>>>(groups, n_groups, N1, n_items, tw);                         \
+        LAUNCHED();                                                                                 \
+        return;                                                                                     \
+    }
+        TDG_MENU(X)
+#undef X
+    }
+    fail(TDG_ERANGE, "corrA: length %d", L);
+}
+
+void launch_corrB(int L, bool write_xc, cudaStream_t st, const tdg::CorrPairOut* pairs, int n_pairs, int N2,
+                  uint32_t W, float inv_n, const float2* tw) {
+    const int n_tiles = (N2 + tdg::kTileB - 1) / tdg::kTileB;
+    const int n_items = n_pairs * n_tiles;
+    switch (L) {
+#define X(LL, P, Q)                                                                                 \
+    case LL: {                                                                                      \
+        using C = tdg::PassB2<P, Q>;                                                                \
+        if (write_xc) {                                                                             \
+            auto* k = tdg::k_corr_passB2<P, Q, true>;                                               \
+            const int grid = persistent_grid(k, C::NT, C::SMEM, n_items);                           \
+            k<<<grid, C::NT, C::SMEM, st>>>(pairs, n_tiles, N2, W, inv_n, n_items, tw);             \
+        } else {                                                                                    \
+            auto* k = tdg::k_corr_passB2<P, Q, false>;                                              \
+            const int grid = persistent_grid(k, C::NT, C::SMEM, n_items);                           \
+            k<<<grid, C::NT, C::SMEM, st>>>(pairs, n_tiles, N2, W, inv_n, n_items, tw);             \
+        }                                                                                           \
+        LAUNCHED();                                                                                 \
+        return;                                                                                     \
+    }
+        TDG_MENU(X)
+#undef X
+    }
+    fail(TDG_ERANGE, "corrB: length %d", L);
+}
+
+// ---------------------------------------------------------------------------
+// Demodulation filter design, restated from proj/src/dsp.cpp:37-73 with the
+// same float/double arithmetic (fill_bandpass, fill_matched, convolve_into).
+using cfloat = std::complex<float>;
+
+void fill_bandpass(double center, double width, size_t taps, double fs, std::vector<cfloat>& out) {
+    const double pi = 3.14159265358979323846;
+    double fc = width / 2.0;
+    double mid = double(taps - 1) / 2.0;
+    std::vector<double> lp(taps);
+    double sum = 0.0;
+    for (size_t k = 0; k < taps; ++k) {
+        double t = double(k) - mid;
+        double x = 2.0 * fc * t / fs;
+        double sinc = (x == 0.0) ? 1.0 : std::sin(pi * x) / (pi * x);
+        double w = (taps == 1) ? 1.0 : 0.54 - 0.46 * std::cos(2.0 * pi * double(k) / double(taps - 1));
+        lp[k] = sinc * w;
+        sum += lp[k];
+    }
+    out.resize(taps);
+    for (size_t k = 0; k < taps; ++k) {
+        double t = double(k) - mid;
+        double a = 2.0 * pi * center * t / fs;
+        double g = lp[k] / sum;
+        out[k] = cfloat(float(g * std::cos(a)), float(g * std::sin(a)));
+    }
+}
+
+void fill_matched(double freq, size_t spb, double fs, std::vector<cfloat>& out) {
+    const double pi = 3.14159265358979323846;
+    out.resize(spb);
+    for (size_t k = 0; k < spb; ++k) {
+        double a = 2.0 * pi * freq * double(spb - 1 - k) / fs;
+        out[k] = cfloat(float(std::cos(a)), float(-std::sin(a)));
+    }
+}
+
+std::vector<cfloat> convolve(const std::vector<cfloat>& a, const std::vector<cfloat>& b) {
+    std::vector<cfloat> out(a.size() + b.size() - 1, cfloat{0.0f, 0.0f});
+    for (size_t i = 0; i < a.size(); ++i)
+        for (size_t j = 0; j < b.size(); ++j) out[i + j] += a[i] * b[j];
+    return out;
+}
+
+size_t samples_per_bit(const tdg_modulation& m) {
+    double spb = m.sample_rate / m.bit_rate;
+    auto n = static_cast<size_t>(spb + 0.5);
+    if (n < 1 || std::abs(spb - double(n)) > 1e-9)
+        fail(TDG_EINVAL, "sample_rate / bit_rate must be a positive integer");
+    return n;
+}
+
+void validate_cfg(const tdg_demod_config& c) {
+    if (c.bandpass_taps < 1) fail(TDG_EINVAL, "design_bandpass: taps must be >= 1");
+    if (c.bandpass_width <= 0.0) fail(TDG_EINVAL, "design_bandpass: width must be positive");
+    if (std::abs(c.bandpass_center) + c.bandpass_width / 2.0 > c.mod.sample_rate / 2.0)
+        fail(TDG_EINVAL, "design_bandpass: band outside Nyquist");
+    samples_per_bit(c.mod);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+struct tdg_ctx;
+struct KScope {   // records a CUDA event pair around one launch when timing is on
+    tdg_ctx* ctx;
+    const char* name;
+    cudaEvent_t a = nullptr;
+    KScope(tdg_ctx* c, const char* n);
+    ~KScope();
+};
+
+struct tdg_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::map<int, std::unique_ptr<DevBuf>> tw;   // per pass length: w_L^{+a c}, index a*Q + c
+    // filter spectra cache
+    std::string hkey;
+    DevBuf hspec;
+    int clen = 0;
+    // scratch
+    DevBuf T, M, keys, det_dev, stream_buf;
+    DescPack pk_fwd, pk_corr, pk_misc;
+    std::vector<char> host_stage;
+    int64_t wave_pairs = 8;      // correlation pairs per pass-A/pass-B wave
+    int64_t fwd_wave = 8;        // sequence pairs per forward-FFT wave
+    // optional per-launch CUDA-event timing (bench.py roofline)
+    bool time_kernels = false;
+    struct KTime {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<KTime> ktimes;
+    std::vector<cudaEvent_t> ev_pool;
+    std::map<std::string, std::pair<uint64_t, double>> kstats;   // name -> (count, total ms)
+    cudaEvent_t ev() {
+        if (ev_pool.empty()) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            return e;
+        }
+        cudaEvent_t e = ev_pool.back();
+        ev_pool.pop_back();
+        return e;
+    }
+    void collect() {
+        if (ktimes.empty()) return;
+        CK(cudaStreamSynchronize(stream));
+        for (auto& k : ktimes) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, k.a, k.b));
+            auto& st = kstats[k.name];
+            st.first += 1;
+            st.second += ms;
+            ev_pool.push_back(k.a);
+            ev_pool.push_back(k.b);
+        }
+        ktimes.clear();
+    }
+
+    const float2* twiddles(int L) {
+        auto it = tw.find(L);
+        if (it != tw.end()) return it->second->as<float2>();
+        const PassShape& s = shape_of(L);
+        std::vector<float2> h(static_cast<size_t>(L));
+        const double pi = 3.14159265358979323846;
+        for (int a = 0; a < s.P; ++a)
+            for (int c = 0; c < s.Q; ++c) {
+                const long e = long(a) * c % L;
+                const double ang = 2.0 * pi * double(e) / double(L);
+                h[size_t(a) * s.Q + c] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
+            }
+        auto buf = std::make_unique<DevBuf>();
+        buf->ensure(h.size() * sizeof(float2));
+        CK(cudaMemcpy(buf->p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice));
+        const float2* p = buf->as<float2>();
+        tw[L] = std::move(buf);
+        return p;
+    }
+
+    // single-array upload through a pack
+    template <class T>
+    T* upload(DescPack& pk, const std::vector<T>& v) {
+        pk.begin();
+        const size_t off = pk.add(v);
+        pk.commit(stream);
+        return pk.at<T>(off);
+    }
+
+    // FFT_1024 spectra of the LO-shifted composed filters for a bin set.
+    const float2* filter_spectra(const tdg_demod_config& c, const std::vector<double>& bins) {
+        validate_cfg(c);
+        char key[256];
+        snprintf(key, sizeof(key), "%.17g/%.17g/%.17g/%.17g/%llu/%.17g/%.17g/%llu|", c.mod.sample_rate, c.mod.bit_rate,
+                 c.mod.freq_one, c.mod.freq_zero, (unsigned long long)c.mod.packet_bits, c.bandpass_center,
+                 c.bandpass_width, (unsigned long long)c.bandpass_taps);
+        std::string k(key);
+        for (double b : bins) {
+            snprintf(key, sizeof(key), "%.17g,", b);
+            k += key;
+        }
+        if (k == hkey) return hspec.as<float2>();
+        const size_t spb = samples_per_bit(c.mod);
+        std::vector<cfloat> hbp, hm;
+        fill_bandpass(c.bandpass_center, c.bandpass_width, size_t(c.bandpass_taps), c.mod.sample_rate, hbp);
+        fill_matched(c.mod.freq_one, spb, c.mod.sample_rate, hm);
+        const auto h1c = convolve(hbp, hm);
+        fill_matched(c.mod.freq_zero, spb, c.mod.sample_rate, hm);
+        const auto h0c = convolve(hbp, hm);
+        clen = int(h1c.size());
+        if (clen > 1024 - 32) fail(TDG_ERANGE, "composed filter of %d taps exceeds the 1024-point demod block", clen);
+        const double pi = 3.14159265358979323846;
+        std::vector<float2> H(bins.size() * 2 * 1024);
+        std::vector<std::complex<double>> tw(1024);
+        for (int k = 0; k < 1024; ++k) tw[size_t(k)] = std::polar(1.0, -2.0 * pi * k / 1024.0);
+        for (size_t b = 0; b < bins.size(); ++b) {
+            const double om = 2.0 * pi * bins[b] / c.mod.sample_rate;
+            for (int f = 0; f < 2; ++f) {
+                const auto& h = f == 0 ? h1c : h0c;
+                std::vector<std::complex<double>> hb(h.size());
+                for (size_t j = 0; j < h.size(); ++j)
+                    hb[j] = std::complex<double>(h[j].real(), h[j].imag()) * std::polar(1.0, om * double(j));
+                for (int kk = 0; kk < 1024; ++kk) {
+                    std::complex<double> acc = 0.0;
+                    for (size_t j = 0; j < h.size(); ++j) acc += hb[j] * tw[(size_t(kk) * j) % 1024];
+                    H[(b * 2 + size_t(f)) * 1024 + size_t(kk)] = make_float2(float(acc.real()), float(acc.imag()));
+                }
+            }
+        }
+        hspec.ensure(H.size() * sizeof(float2));
+        CK(cudaMemcpy(hspec.p, H.data(), H.size() * sizeof(float2), cudaMemcpyHostToDevice));
+        hkey = k;
+        return hspec.as<float2>();
+    }
+};
+
+KScope::KScope(tdg_ctx* c, const char* n) : ctx(c), name(n) {
+    if (ctx->time_kernels) {
+        a = ctx->ev();
+        cudaEventRecord(a, ctx->stream);
+    }
+}
+KScope::~KScope() {
+    if (a) {
+        cudaEvent_t b = ctx->ev();
+        cudaEventRecord(b, ctx->stream);
+        ctx->ktimes.push_back({name, a, b});
+    }
+}
+
+struct tdg_codeset {
+    tdg_ctx* ctx = nullptr;    // creating context (not owned; may be destroyed first)
+    int device = 0;
+    uint64_t window_len = 0;
+    uint64_t n_codes = 0;
+    int N1 = 0, N2 = 0;
+    uint64_t H = 0;            // half-column spectrum length (N1/2+1)*N2
+    uint64_t rep_cap = 0;      // replica_d stride
+    DevBuf spec, rep, nlen_dev, energy_dev, abs_dev;
+    std::vector<uint64_t> nlen;
+    std::vector<float> energy, abs_sum;
+    uint64_t corr_len() const { return uint64_t(N1) * uint64_t(N2); }
+};
+
+struct tdg_windows {
+    tdg_ctx* ctx = nullptr;    // creating context (not owned; may be destroyed first)
+    int device = 0;
+    uint64_t W = 0, n_windows = 0, n_bins = 0;
+    DevBuf d, u;
+    std::vector<int64_t> start;   // window_start per slot
+    DevBuf dspec;
+    uint64_t dspec_N = 0;         // transform length dspec was computed for (0 = stale)
+    uint64_t slots() const { return n_windows * n_bins; }
+};
+
+namespace {
+
+// Forward transforms of real sequences (pairs packed as r1 + i r2) into
+// Hermitian half-column spectra.
+struct FwdJob {
+    const float* r1;
+    const float* r2;
+    uint64_t len1, len2;
+    float2* S1;
+    float2* S2;
+};
+
+// split = true: r1, r2 -> two Hermitian half-column spectra (window d's).
+// split = false: the packed pair's full spectrum X (code pairs), into S1.
+void run_forward(tdg_ctx* ctx, int N1, int N2, const std::vector<FwdJob>& jobs, bool split) {
+    const uint64_t N = uint64_t(N1) * uint64_t(N2);
+    const float2* tw1 = ctx->twiddles(N1);
+    const float2* tw2 = ctx->twiddles(N2);
+    const size_t wave = size_t(std::max<int64_t>(1, ctx->fwd_wave));
+    ctx->T.ensure(wave * N * sizeof(float2));
+    std::vector<tdg::SeqPairDesc> d(jobs.size());
+    for (size_t i = 0; i < jobs.size(); ++i) {
+        const auto& j = jobs[i];
+        d[i] = {j.r1, j.r2, j.len1, j.len2, ctx->T.as<float2>() + (i % wave) * N, j.S1, j.S2};
+    }
+    tdg::SeqPairDesc* dd = ctx->upload(ctx->pk_fwd, d);
+    for (size_t base = 0; base < jobs.size(); base += wave) {
+        const size_t n = std::min(wave, jobs.size() - base);
+        {
+            KScope ks(ctx, "fwd_pass1");
+            launch_fwd1(N1, dim3(unsigned((N2 + kTB - 1) / kTB), unsigned(n)), ctx->stream, dd + base, N2, tw1);
+        }
+        {
+            KScope ks(ctx, "fwd_pass2");
+            launch_fwd2(N2, split, dim3(unsigned(N1 / 2 + 1), unsigned(n)), ctx->stream, dd + base, N1, tw2);
+        }
+    }
+}
+
+void ensure_dspec(tdg_ctx* ctx, tdg_windows* w, int N1, int N2) {
+    const uint64_t N = uint64_t(N1) * uint64_t(N2);
+    if (w->dspec_N == N) return;
+    const uint64_t H = uint64_t(N1 / 2 + 1) * uint64_t(N2);
+    w->dspec.ensure(w->slots() * H * sizeof(float2));
+    std::vector<FwdJob> jobs;
+    for (uint64_t s = 0; s < w->slots(); s += 2) {
+        const bool two = s + 1 < w->slots();
+        jobs.push_back({w->d.as<float>() + s * w->W, two ? w->d.as<float>() + (s + 1) * w->W : nullptr, w->W,
+                        two ? w->W : 0, w->dspec.as<float2>() + s * H, two ? w->dspec.as<float2>() + (s + 1) * H : nullptr});
+    }
+    run_forward(ctx, N1, N2, jobs, true);
+    w->dspec_N = N;
+}
+
+// Correlation jobs: each is one stored code pair (codes 2p, 2p+1) against
+// one window slot; outputs are argmax keys and/or full xc rows.
+struct CorrJob {
+    uint64_t slot;
+    uint64_t pair;
+    unsigned long long* key_a;
+    unsigned long long* key_b;   // nullptr if the pair has one code
+    float* xc_a;                 // diagnostic outputs (nullable)
+    float* xc_b;
+};
+
+void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const std::vector<CorrJob>& jobs,
+                      bool write_xc) {
+    const int N1 = cs->N1, N2 = cs->N2;
+    const uint64_t N = cs->corr_len(), H = cs->H;
+    ensure_dspec(ctx, w, N1, N2);
+    const float2* twA = ctx->twiddles(N2);
+    const float2* twB = ctx->twiddles(N1);
+    const size_t wave = size_t(std::max<int64_t>(kG, ctx->wave_pairs / kG * kG));
+    const uint64_t n_tiles = uint64_t((N2 + tdg::kTileB - 1) / tdg::kTileB);
+    const uint64_t Mstride = n_tiles * uint64_t(N1) * tdg::kTileB;   // tile-major M per pair
+    ctx->M.ensure(wave * Mstride * sizeof(float2));
+    std::vector<tdg::CorrGroup<kG>> groups;
+    std::vector<tdg::CorrPairOut> outs(jobs.size());
+    std::vector<size_t> wave_group0;   // first group index of each wave
+    for (size_t base = 0; base < jobs.size(); base += wave) {
+        const size_t n = std::min(wave, jobs.size() - base);
+        wave_group0.push_back(groups.size());
+        for (size_t i = 0; i < n; ++i) {
+            const CorrJob& jb = jobs[base + i];
+            float2* M = ctx->M.as<float2>() + i * Mstride;
+            const float2* D = w->dspec.as<float2>() + jb.slot * H;
+            if (groups.size() == wave_group0.back() || groups.back().npairs == kG || groups.back().D != D) {
+                tdg::CorrGroup<kG> g{};
+                g.D = D;
+                g.npairs = 0;
+                groups.push_back(g);
+            }
+            auto& g = groups.back();
+            g.Ca[g.npairs] = cs->spec.as<float2>() + jb.pair * N;
+            g.Cb[g.npairs] = nullptr;
+            g.M[g.npairs] = M;
+            ++g.npairs;
+            auto& o = outs[base + i];
+            o.M = M;
+            o.key_a = jb.key_a;
+            o.key_b = jb.key_b;
+            o.xc_a = jb.xc_a;
+            o.xc_b = jb.xc_b;
+        }
+    }
+    wave_group0.push_back(groups.size());
+    ctx->pk_corr.begin();
+    const size_t og = ctx->pk_corr.add(groups);
+    const size_t oo = ctx->pk_corr.add(outs);
+    ctx->pk_corr.commit(ctx->stream);
+    auto* gd = ctx->pk_corr.at<tdg::CorrGroup<kG>>(og);
+    auto* od = ctx->pk_corr.at<tdg::CorrPairOut>(oo);
+    for (size_t wv = 0, base = 0; base < jobs.size(); ++wv, base += wave) {
+        const size_t n = std::min(wave, jobs.size() - base);
+        const size_t g0 = wave_group0[wv], g1 = wave_group0[wv + 1];
+        {
+            KScope ks(ctx, "corr_passA");
+            launch_corrA(N2, ctx->stream, gd + g0, int(g1 - g0), N1, twA);
+        }
+        {
+            KScope ks(ctx, "corr_passB");
+            launch_corrB(N1, write_xc, ctx->stream, od + base, int(n), N2, uint32_t(w->W), 1.0f / float(N), twB);
+        }
+    }
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* tdg_last_error(void) { return g_err.c_str(); }
+const char* tdg_version(void) { return "tagdsp_gpu 0.1 (sm_100a)"; }
+uint64_t tdg_kernel_launches(void) { return g_launches.load(); }
+
+int tdg_ctx_create(int device, tdg_ctx** out) {
+    return guard([&] {
+        *out = nullptr;
+        CK(cudaSetDevice(device));
+        auto ctx = std::make_unique<tdg_ctx>();
+        ctx->device = device;
+        CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        *out = ctx.release();
+    });
+}
+
+void tdg_ctx_destroy(tdg_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& k : ctx->ktimes) {
+        cudaEventDestroy(k.a);
+        cudaEventDestroy(k.b);
+    }
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int tdg_ctx_synchronize(tdg_ctx* ctx) {
+    return guard([&] { CK(cudaStreamSynchronize(ctx->stream)); });
+}
+
+void* tdg_ctx_stream(tdg_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+uint64_t tdg_pad_length(uint64_t n) {
+    uint64_t r = 0;
+    if (guard([&] { r = pad_length_impl(n); })) return 0;
+    return r;
+}
+
+uint64_t tdg_corr_len(uint64_t window_len, uint64_t nonzero_len) {
+    int n1, n2;
+    const uint64_t need = std::max<uint64_t>(1, window_len + nonzero_len - (nonzero_len ? 1 : 0));
+    if (!choose_corr_len(need, &n1, &n2)) return 0;
+    return uint64_t(n1) * uint64_t(n2);
+}
+
+int tdg_kernel_time(tdg_ctx* ctx, const char* name, uint64_t* count, double* total_ms) {
+    return guard([&] {
+        ctx->collect();
+        auto it = ctx->kstats.find(name);
+        *count = it == ctx->kstats.end() ? 0 : it->second.first;
+        *total_ms = it == ctx->kstats.end() ? 0.0 : it->second.second;
+    });
+}
+
+int tdg_kernel_time_reset(tdg_ctx* ctx) {
+    return guard([&] {
+        ctx->collect();
+        ctx->kstats.clear();
+    });
+}
+
+int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
+    return guard([&] {
+        std::string k(key);
+        if (k == "time_kernels") {
+            ctx->collect();
+            ctx->time_kernels = value != 0;
+        } else if (k == "wave_pairs")
+            ctx->wave_pairs = value > 0 ? value : 8;
+        else if (k == "fwd_wave")
+            ctx->fwd_wave = value > 0 ? value : 8;
+        else
+            fail(TDG_EINVAL, "unknown option %s", key);
+    });
+}
+
+// ---- code sets -------------------------------------------------------------
+namespace {
+
+void finish_codeset(tdg_ctx* ctx, tdg_codeset* cs, const float* d, const float* u, uint64_t stride,
+                    const std::vector<uint64_t>& lens, uint64_t ref_corr_len) {
+    const uint64_t n = cs->n_codes;
+    cs->nlen_dev.ensure(n * sizeof(uint64_t));
+    cs->energy_dev.ensure(n * sizeof(float));
+    cs->abs_dev.ensure(n * sizeof(float));
+    cs->rep_cap = 0;
+    for (uint64_t l : lens) cs->rep_cap = std::max(cs->rep_cap, l);
+    cs->rep_cap = std::max<uint64_t>(cs->rep_cap, 1);
+    cs->rep.ensure(n * cs->rep_cap * sizeof(float));
+    std::vector<tdg::SupportDesc> sd(n);
+    for (uint64_t i = 0; i < n; ++i)
+        sd[i] = {d + i * stride, u ? u + i * stride : nullptr, lens[i], cs->rep.as<float>() + i * cs->rep_cap,
+                 cs->rep_cap, cs->nlen_dev.as<uint64_t>() + i, cs->energy_dev.as<float>() + i, cs->abs_dev.as<float>() + i};
+    auto* sdd = ctx->upload(ctx->pk_misc, sd);
+    tdg::k_support<<<unsigned(n), 1024, 0, ctx->stream>>>(sdd);
+    LAUNCHED();
+    cs->nlen.resize(n);
+    cs->energy.resize(n);
+    cs->abs_sum.resize(n);
+    CK(cudaMemcpyAsync(cs->nlen.data(), cs->nlen_dev.p, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(cs->energy.data(), cs->energy_dev.p, n * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(cs->abs_sum.data(), cs->abs_dev.p, n * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    uint64_t nmax = 1;
+    for (uint64_t i = 0; i < n; ++i) {
+        // make_transformed precondition (proj/src/detector.cpp:28-29)
+        if (cs->window_len + cs->nlen[i] > ref_corr_len + 1)
+            fail(TDG_EINVAL, "make_transformed: transform too short for linear correlation");
+        nmax = std::max(nmax, cs->nlen[i]);
+    }
+    if (cs->window_len >= (uint64_t(1) << 32)) fail(TDG_ERANGE, "window_len too large");
+    if (!choose_corr_len(cs->window_len + nmax - 1, &cs->N1, &cs->N2))
+        fail(TDG_ERANGE, "window_len + support %llu exceeds the largest supported transform",
+             (unsigned long long)(cs->window_len + nmax));
+    cs->H = uint64_t(cs->N1 / 2 + 1) * uint64_t(cs->N2);
+    const uint64_t N = cs->corr_len();
+    const uint64_t npairs = (n + 1) / 2;
+    cs->spec.ensure(npairs * N * sizeof(float2));
+    std::vector<FwdJob> jobs;
+    for (uint64_t i = 0; i < n; i += 2) {
+        const bool two = i + 1 < n;
+        jobs.push_back({cs->rep.as<float>() + i * cs->rep_cap, two ? cs->rep.as<float>() + (i + 1) * cs->rep_cap : nullptr,
+                        cs->nlen[i], two ? cs->nlen[i + 1] : 0, cs->spec.as<float2>() + (i / 2) * N, nullptr});
+    }
+    run_forward(ctx, cs->N1, cs->N2, jobs, false);
+    CK(cudaStreamSynchronize(ctx->stream));
+}
+
+void demod_launch(tdg_ctx* ctx, const void* in, bool int16_input, uint64_t in_len,
+                  const std::vector<tdg::DemodWindowDesc>& wins, uint64_t W, int n_bins, uint64_t slot_stride,
+                  const float2* H, float eps) {
+    if (W == 0 || wins.empty()) return;
+    const int V = 1024 - (ctx->clen - 1);
+    const uint64_t nblocks = (W + uint64_t(V) - 1) / uint64_t(V);
+    dim3 grid(unsigned((nblocks + kDemodBlk - 1) / kDemodBlk), unsigned(wins.size()));
+    const size_t sm = size_t(kDemodBlk) * (1024 + 32 * 33) * sizeof(float2) + size_t(kDemodBlk) * 1024 * sizeof(float);
+    const float2* tw = ctx->twiddles(1024);
+    auto* wd = ctx->upload(ctx->pk_misc, wins);
+    KScope ks(ctx, "demod");
+    if (int16_input) {
+        set_smem(tdg::k_demod<int32_t, kDemodBlk>, sm);
+        tdg::k_demod<int32_t, kDemodBlk><<<grid, kDemodBlk * 32, sm, ctx->stream>>>(
+            static_cast<const int32_t*>(in), in_len, wd, uint32_t(W), ctx->clen, n_bins, slot_stride, H, eps, tw);
+    } else {
+        set_smem(tdg::k_demod<float2, kDemodBlk>, sm);
+        tdg::k_demod<float2, kDemodBlk><<<grid, kDemodBlk * 32, sm, ctx->stream>>>(
+            static_cast<const float2*>(in), in_len, wd, uint32_t(W), ctx->clen, n_bins, slot_stride, H, eps, tw);
+    }
+    LAUNCHED();
+}
+
+}  // namespace
+
+int tdg_codeset_prepare(tdg_ctx* ctx, const tdg_demod_config* cfg, uint64_t window_len, const uint8_t* bits,
+                        uint64_t n_codes, tdg_codeset** out) {
+    return guard([&] {
+        *out = nullptr;
+        CK(cudaSetDevice(ctx->device));
+        const tdg_demod_config& c = *cfg;
+        validate_cfg(c);
+        const uint64_t spb = samples_per_bit(c.mod);
+        const uint64_t nbits = c.mod.packet_bits;
+        const uint64_t psamp = nbits * spb;
+        if (window_len < psamp) fail(TDG_EINVAL, "prepare_code: window shorter than a packet");
+        if (n_codes == 0) fail(TDG_EINVAL, "prepare_code: no codes");
+        const uint64_t clen_ref = c.bandpass_taps + spb - 1;
+        const uint64_t ref_corr = pad_length_impl(window_len + psamp + clen_ref);
+        // filters for lo = 0 (replicas skip the local oscillator, proj/src/detector.cpp:59-61)
+        const float2* H = ctx->filter_spectra(c, std::vector<double>{0.0});
+        // replica demod span: the packet plus the filter tail plus one block of margin
+        const uint64_t Wr = std::min<uint64_t>(window_len, psamp + uint64_t(ctx->clen) + 1024);
+        auto cs = std::make_unique<tdg_codeset>();
+        cs->ctx = ctx;
+        cs->device = ctx->device;
+        cs->window_len = window_len;
+        cs->n_codes = n_codes;
+        DevBuf dbits, drep, dd, du;
+        dbits.ensure(n_codes * nbits);
+        CK(cudaMemcpyAsync(dbits.p, bits, n_codes * nbits, cudaMemcpyHostToDevice, ctx->stream));
+        drep.ensure(n_codes * Wr * sizeof(float2));
+        const double pi = 3.14159265358979323846;
+        const double step1 = 2.0 * pi * c.mod.freq_one / c.mod.sample_rate;
+        const double step0 = 2.0 * pi * c.mod.freq_zero / c.mod.sample_rate;
+        tdg::k_synth_replica<<<unsigned(n_codes), 1024, nbits * sizeof(uint32_t), ctx->stream>>>(
+            dbits.as<uint8_t>(), uint32_t(nbits), uint32_t(spb), step1, step0, drep.as<float2>(), Wr);
+        LAUNCHED();
+        dd.ensure(n_codes * Wr * sizeof(float));
+        du.ensure(n_codes * Wr * sizeof(float));
+        std::vector<tdg::DemodWindowDesc> wins(n_codes);
+        for (uint64_t i = 0; i < n_codes; ++i) wins[i] = {i * Wr, dd.as<float>() + i * Wr, du.as<float>() + i * Wr};
+        demod_launch(ctx, drep.p, false, n_codes * Wr, wins, Wr, 1, Wr, H, c.eps);
+        std::vector<uint64_t> lens(n_codes, Wr);
+        finish_codeset(ctx, cs.get(), dd.as<float>(), du.as<float>(), Wr, lens, ref_corr);
+        *out = cs.release();
+    });
+}
+
+int tdg_codeset_from_replicas(tdg_ctx* ctx, uint64_t window_len, uint64_t corr_len, const float* const* replica_d,
+                              const float* const* replica_u, const uint64_t* lengths, uint64_t n_codes,
+                              tdg_codeset** out) {
+    return guard([&] {
+        *out = nullptr;
+        CK(cudaSetDevice(ctx->device));
+        if (n_codes == 0) fail(TDG_EINVAL, "make_transformed: no codes");
+        uint64_t stride = 1;
+        for (uint64_t i = 0; i < n_codes; ++i) stride = std::max(stride, lengths[i]);
+        std::vector<float> hd(n_codes * stride, 0.f), hu;
+        const bool have_u = replica_u != nullptr;
+        if (have_u) hu.assign(n_codes * stride, 0.f);
+        std::vector<uint64_t> lens(n_codes);
+        for (uint64_t i = 0; i < n_codes; ++i) {
+            lens[i] = lengths[i];
+            std::memcpy(hd.data() + i * stride, replica_d[i], lengths[i] * sizeof(float));
+            if (have_u && replica_u[i]) std::memcpy(hu.data() + i * stride, replica_u[i], lengths[i] * sizeof(float));
+            else if (have_u) std::memcpy(hu.data() + i * stride, replica_d[i], lengths[i] * sizeof(float));
+        }
+        auto cs = std::make_unique<tdg_codeset>();
+        cs->ctx = ctx;
+        cs->device = ctx->device;
+        cs->window_len = window_len;
+        cs->n_codes = n_codes;
+        DevBuf dd, du;
+        dd.ensure(hd.size() * sizeof(float));
+        CK(cudaMemcpy(dd.p, hd.data(), hd.size() * sizeof(float), cudaMemcpyHostToDevice));
+        if (have_u) {
+            du.ensure(hu.size() * sizeof(float));
+            CK(cudaMemcpy(du.p, hu.data(), hu.size() * sizeof(float), cudaMemcpyHostToDevice));
+        }
+        finish_codeset(ctx, cs.get(), dd.as<float>(), have_u ? du.as<float>() : nullptr, stride, lens, corr_len);
+        *out = cs.release();
+    });
+}
+
+void tdg_codeset_destroy(tdg_codeset* cs) {
+    if (!cs) return;
+    cudaSetDevice(cs->device);   // cudaFree in the buffers' destructors synchronises
+    delete cs;
+}
+
+uint64_t tdg_codeset_size(const tdg_codeset* cs) { return cs ? cs->n_codes : 0; }
+
+int tdg_codeset_info(const tdg_codeset* cs, uint64_t idx, uint64_t* nonzero_len, float* energy, float* abs_sum,
+                     uint64_t* corr_len) {
+    return guard([&] {
+        if (idx >= cs->n_codes) fail(TDG_EINVAL, "code index out of range");
+        if (nonzero_len) *nonzero_len = cs->nlen[idx];
+        if (energy) *energy = cs->energy[idx];
+        if (abs_sum) *abs_sum = cs->abs_sum[idx];
+        if (corr_len) *corr_len = cs->corr_len();
+    });
+}
+
+int tdg_codeset_replica(const tdg_codeset* cs, uint64_t idx, float* replica_d_out) {
+    return guard([&] {
+        if (idx >= cs->n_codes) fail(TDG_EINVAL, "code index out of range");
+        CK(cudaSetDevice(cs->device));
+        CK(cudaDeviceSynchronize());
+        CK(cudaMemcpy(replica_d_out, cs->rep.as<float>() + idx * cs->rep_cap, cs->nlen[idx] * sizeof(float),
+                      cudaMemcpyDeviceToHost));
+    });
+}
+
+// ---- windows ---------------------------------------------------------------
+int tdg_windows_create(tdg_ctx* ctx, uint64_t window_len, uint64_t n_windows, uint64_t n_bins, tdg_windows** out) {
+    return guard([&] {
+        *out = nullptr;
+        CK(cudaSetDevice(ctx->device));
+        if (window_len == 0 || n_windows == 0 || n_bins == 0) fail(TDG_EINVAL, "windows: empty shape");
+        if (window_len >= (uint64_t(1) << 32)) fail(TDG_ERANGE, "window_len too large");
+        auto w = std::make_unique<tdg_windows>();
+        w->ctx = ctx;
+        w->device = ctx->device;
+        w->W = window_len;
+        w->n_windows = n_windows;
+        w->n_bins = n_bins;
+        w->d.ensure(w->slots() * window_len * sizeof(float));
+        w->u.ensure(w->slots() * window_len * sizeof(float));
+        CK(cudaMemsetAsync(w->d.p, 0, w->d.bytes, ctx->stream));
+        CK(cudaMemsetAsync(w->u.p, 0, w->u.bytes, ctx->stream));
+        w->start.assign(w->slots(), 0);
+        *out = w.release();
+    });
+}
+
+void tdg_windows_destroy(tdg_windows* w) {
+    if (!w) return;
+    cudaSetDevice(w->device);
+    delete w;
+}
+
+namespace {
+void demodulate_impl(tdg_ctx* ctx, tdg_windows* win, const tdg_demod_config* cfg, const double* lo_bins,
+                     uint64_t n_bins, const int16_t* iq_dev, uint64_t n_complex, int64_t stream_start,
+                     uint64_t advance, uint64_t n_windows) {
+    if (n_bins != win->n_bins) fail(TDG_EINVAL, "demodulate: bin count %llu != window set's %llu",
+                                    (unsigned long long)n_bins, (unsigned long long)win->n_bins);
+    if (n_windows > win->n_windows) fail(TDG_EINVAL, "demodulate: too many windows");
+    if (n_windows && (n_windows - 1) * advance + win->W > n_complex)
+        fail(TDG_EINVAL, "demodulate: windows exceed the sample block");
+    std::vector<double> bins(lo_bins, lo_bins + n_bins);
+    const float2* H = ctx->filter_spectra(*cfg, bins);
+    std::vector<tdg::DemodWindowDesc> wins(n_windows);
+    for (uint64_t w = 0; w < n_windows; ++w) {
+        const uint64_t slot0 = w * n_bins;
+        wins[w] = {w * advance, win->d.as<float>() + slot0 * win->W, win->u.as<float>() + slot0 * win->W};
+        for (uint64_t b = 0; b < n_bins; ++b) win->start[slot0 + b] = stream_start + int64_t(w * advance);
+    }
+    demod_launch(ctx, iq_dev, true, n_complex, wins, win->W, int(n_bins), win->W, H, cfg->eps);
+    win->dspec_N = 0;
+}
+}  // namespace
+
+int tdg_demodulate_device(tdg_ctx* ctx, tdg_windows* win, const tdg_demod_config* cfg, const double* lo_bins,
+                          uint64_t n_bins, const int16_t* iq_dev, uint64_t n_complex, int64_t stream_start,
+                          uint64_t advance, uint64_t n_windows) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        demodulate_impl(ctx, win, cfg, lo_bins, n_bins, iq_dev, n_complex, stream_start, advance, n_windows);
+    });
+}
+
+int tdg_demodulate(tdg_ctx* ctx, tdg_windows* win, const tdg_demod_config* cfg, const double* lo_bins,
+                   uint64_t n_bins, const int16_t* iq, uint64_t n_complex, int64_t stream_start, uint64_t advance,
+                   uint64_t n_windows) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        ctx->stream_buf.ensure(std::max<uint64_t>(n_complex, 1) * 2 * sizeof(int16_t));
+        CK(cudaMemcpyAsync(ctx->stream_buf.p, iq, n_complex * 2 * sizeof(int16_t), cudaMemcpyHostToDevice, ctx->stream));
+        demodulate_impl(ctx, win, cfg, lo_bins, n_bins, ctx->stream_buf.as<int16_t>(), n_complex, stream_start, advance,
+                        n_windows);
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int tdg_windows_set_du(tdg_ctx* ctx, tdg_windows* w, uint64_t slot, const float* d, const float* u,
+                       int64_t window_start) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (slot >= w->slots()) fail(TDG_EINVAL, "slot out of range");
+        CK(cudaMemcpyAsync(w->d.as<float>() + slot * w->W, d, w->W * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(w->u.as<float>() + slot * w->W, u, w->W * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        w->start[slot] = window_start;
+        w->dspec_N = 0;
+    });
+}
+
+int tdg_windows_get_du(tdg_ctx* ctx, const tdg_windows* w, uint64_t slot, float* d, float* u) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (slot >= w->slots()) fail(TDG_EINVAL, "slot out of range");
+        CK(cudaStreamSynchronize(ctx->stream));
+        if (d) CK(cudaMemcpy(d, w->d.as<float>() + slot * w->W, w->W * sizeof(float), cudaMemcpyDeviceToHost));
+        if (u) CK(cudaMemcpy(u, w->u.as<float>() + slot * w->W, w->W * sizeof(float), cudaMemcpyDeviceToHost));
+    });
+}
+
+// ---- detection -------------------------------------------------------------
+namespace {
+void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float threshold, double fs, tdg_detection* out) {
+    if (cs->window_len != w->W) fail(TDG_EINVAL, "batch_xcorr: mixed window shapes");
+    for (uint64_t i = 0; i < cs->n_codes; ++i)
+        if (w->W + cs->nlen[i] > cs->corr_len() + 1) fail(TDG_EINVAL, "batch_xcorr: window does not fit transform size");
+    const uint64_t ns = w->slots(), nc = cs->n_codes;
+    ctx->keys.ensure(ns * nc * sizeof(unsigned long long));
+    CK(cudaMemsetAsync(ctx->keys.p, 0, ns * nc * sizeof(unsigned long long), ctx->stream));
+    std::vector<CorrJob> jobs;
+    unsigned long long* keys = ctx->keys.as<unsigned long long>();
+    for (uint64_t s = 0; s < ns; ++s)
+        for (uint64_t p = 0; 2 * p < nc; ++p)
+            jobs.push_back({s, p, keys + s * nc + 2 * p, 2 * p + 1 < nc ? keys + s * nc + 2 * p + 1 : nullptr,
+                            nullptr, nullptr});
+    run_correlations(ctx, w, cs, jobs, false);
+    ctx->det_dev.ensure(ns * nc * sizeof(tdg_detection));
+    std::vector<tdg::StatsDesc> sd(ns * nc);
+    for (uint64_t s = 0; s < ns; ++s)
+        for (uint64_t c = 0; c < nc; ++c) {
+            auto& x = sd[s * nc + c];
+            x.d = w->d.as<float>() + s * w->W;
+            x.u = w->u.as<float>() + s * w->W;
+            x.dc = cs->rep.as<float>() + c * cs->rep_cap;
+            x.key = ctx->keys.as<unsigned long long>() + s * nc + c;
+            x.out = ctx->det_dev.as<tdg_detection>() + s * nc + c;
+            x.nonzero_len = uint32_t(cs->nlen[c]);
+            x.energy = cs->energy[c];
+            x.window_start = w->start[s];
+            x.code_index = int32_t(c);
+            x.bin = int32_t(s % w->n_bins);
+        }
+    auto* sdd = ctx->upload(ctx->pk_misc, sd);
+    KScope ks(ctx, "stats");
+    tdg::k_stats<<<unsigned(ns * nc), 256, 0, ctx->stream>>>(sdd, uint32_t(w->W), fs, threshold);
+    LAUNCHED();
+    if (out) {
+        CK(cudaMemcpyAsync(out, ctx->det_dev.p, ns * nc * sizeof(tdg_detection), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+}
+}  // namespace
+
+int tdg_detect(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float threshold, double sample_rate,
+               tdg_detection* out) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        detect_impl(ctx, w, cs, threshold, sample_rate, out);
+    });
+}
+
+int tdg_batch_xcorr(tdg_ctx* ctx, tdg_windows* w, uint64_t slot, const tdg_codeset* cs, const int64_t* idx,
+                    uint64_t n_idx, float* out) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (slot >= w->slots()) fail(TDG_EINVAL, "slot out of range");
+        if (cs->window_len != w->W) fail(TDG_EINVAL, "batch_xcorr: mixed window shapes");
+        std::vector<int64_t> codes(idx, idx + n_idx);
+        for (int64_t c : codes)
+            if (c < 0 || uint64_t(c) >= cs->n_codes) fail(TDG_EINVAL, "code index out of range");
+        DevBuf xc;
+        xc.ensure(std::max<uint64_t>(1, n_idx) * w->W * sizeof(float));
+        // one job per stored pair touched; rows for the requested codes only
+        std::map<uint64_t, std::pair<float*, float*>> per_pair;
+        for (uint64_t i = 0; i < n_idx; ++i) {
+            const uint64_t c = uint64_t(codes[i]);
+            auto& pp = per_pair[c / 2];
+            (c % 2 ? pp.second : pp.first) = xc.as<float>() + i * w->W;
+        }
+        std::vector<CorrJob> jobs;
+        for (auto& [p, rows] : per_pair) jobs.push_back({slot, p, nullptr, nullptr, rows.first, rows.second});
+        run_correlations(ctx, w, cs, jobs, true);
+        CK(cudaMemcpyAsync(out, xc.p, n_idx * w->W * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int tdg_search(tdg_ctx* ctx, const tdg_demod_config* cfg, const double* lo_bins, uint64_t n_bins, const int16_t* iq,
+               uint64_t n_complex, int64_t stream_start, uint64_t window_len, uint64_t advance, const tdg_codeset* cs,
+               float threshold, tdg_detection* out, uint64_t out_cap, uint64_t* n_out) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (advance == 0) fail(TDG_EINVAL, "search: advance must be positive");
+        const uint64_t n_windows = n_complex >= window_len ? (n_complex - window_len) / advance + 1 : 0;
+        if (n_out) *n_out = n_windows * n_bins * cs->n_codes;
+        if (n_windows == 0) return;
+        if (out_cap < n_windows * n_bins * cs->n_codes) fail(TDG_EINVAL, "search: output capacity too small");
+        tdg_windows* w = nullptr;
+        int rc = tdg_windows_create(ctx, window_len, n_windows, n_bins, &w);
+        if (rc) fail(rc, "%s", g_err.c_str());
+        std::unique_ptr<tdg_windows, void (*)(tdg_windows*)> hold(w, tdg_windows_destroy);
+        ctx->stream_buf.ensure(n_complex * 2 * sizeof(int16_t));
+        CK(cudaMemcpyAsync(ctx->stream_buf.p, iq, n_complex * 2 * sizeof(int16_t), cudaMemcpyHostToDevice, ctx->stream));
+        demodulate_impl(ctx, w, cfg, lo_bins, n_bins, ctx->stream_buf.as<int16_t>(), n_complex, stream_start, advance,
+                        n_windows);
+        detect_impl(ctx, w, cs, threshold, cfg->mod.sample_rate, out);
+    });
+}
+
+}  // extern "C"

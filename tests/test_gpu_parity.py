@@ -1,0 +1,205 @@
+"""GPU parity: the B200 path through the C-ABI against the reference compiled
+in place (oracle/_ref) and brute-force oracles, on the reference's own test
+cases (proj/tests/test_detector.cpp, acceptance.cpp) and the search shape."""
+import numpy as np
+import pytest
+
+from parity import compare_detections, direct_xcorr, near_tie_margin
+
+pytestmark = pytest.mark.gpu
+
+
+def _cs_from(capi, ctx, dcs, W, ref):
+    n = max(len(x) for x in dcs)
+    return capi.CodeSet.from_replicas(ctx, W, ref.pad_length(W + n), dcs, dcs)
+
+
+def test_xcorr_matches_brute_force(gpu_ctx, ref):
+    """test_detector.cpp:110-122: 20 random instances, |err| <= 1e-3 * energy."""
+    from paper_2005_10445_b200 import capi
+    worst = 0.0
+    for trial in range(20):
+        dc = ref.gaussian(100 + trial, 64)
+        d = ref.gaussian(200 + trial, 4096)
+        cs = _cs_from(capi, gpu_ctx, [dc], d.size, ref)
+        w = capi.Windows(gpu_ctx, d.size)
+        w.set_du(0, d, d)
+        got = capi.batch_xcorr(gpu_ctx, w, 0, cs)[0]
+        want = direct_xcorr(d, dc)
+        e = cs.info(0)["energy"]
+        worst = max(worst, float(np.abs(got - want).max() / e))
+    assert worst <= 1e-4, worst
+
+
+def test_batch_xcorr_matches_reference(gpu_ctx, ref):
+    """batch_xcorr (detector.cpp:102-120) on 16 codes (odd/even pairing)."""
+    from paper_2005_10445_b200 import capi
+    W = 2048
+    dcs = [ref.gaussian(8000 + i, 100) for i in range(15)]
+    d = ref.gaussian(8999, W)
+    cs = _cs_from(capi, gpu_ctx, dcs, W, ref)
+    w = capi.Windows(gpu_ctx, W)
+    w.set_du(0, d, d)
+    got = capi.batch_xcorr(gpu_ctx, w, 0, cs)
+    s = ref.Session()
+    idx = [s.make_transformed(x, x, W, ref.pad_length(W + 100)) for x in dcs]
+    want = s.batch_xcorr(d, idx)
+    for i in range(len(dcs)):
+        e = cs.info(i)["energy"]
+        assert np.abs(got[i] - want[i]).max() <= 1e-5 * e
+
+
+def test_autocorrelation_peak_is_energy(gpu_ctx, ref):
+    """test_detector.cpp:89-99."""
+    from paper_2005_10445_b200 import capi
+    dc = ref.gaussian(5, 512)
+    d = np.zeros(2048, np.float32)
+    d[:512] = dc
+    cs = _cs_from(capi, gpu_ctx, [dc], 2048, ref)
+    w = capi.Windows(gpu_ctx, 2048)
+    w.set_du(0, d, d)
+    det = capi.detect(gpu_ctx, w, cs, 0.25, 1.0)[0]
+    assert det["peak_index"] == 0
+    assert abs(det["peak_value"] - cs.info(0)["energy"]) <= 1e-4 * cs.info(0)["energy"]
+
+
+def test_demodulate_matches_reference_default_cfg(gpu_ctx, ref):
+    """demodulate_window on a default-config search window, with LO bins."""
+    from paper_2005_10445_b200 import capi
+    from paper_2005_10445_b200._abi import demod_config
+    cfg = demod_config()
+    bits = ref.gen_code(1000, cfg)
+    W = 200000
+    iq = ref.channel_window(bits, cfg, 1000.25, W, 3, snr_db=10.0, freq_offset=50e3)
+    bins = [0.0, 100e3, -100e3]
+    win = capi.Windows(gpu_ctx, W, 1, len(bins))
+    win.demodulate(cfg, bins, iq, stream_start=12345, advance=W, n_windows=1)
+    for b, lo in enumerate(bins):
+        c = demod_config(lo_freq=lo)
+        d_ref, u_ref = ref.demodulate_window(iq, 12345, c)
+        d, u = win.get_du(b)
+        assert np.abs(u - u_ref).max() <= 1e-4 * np.abs(u_ref).max(), lo
+        # d = u / (|f1| + |f0|) is 0/0 rounding dust where the filter output
+        # vanishes (the causal start of the window); compare it where the
+        # denominator is at least 1e-3 of its maximum
+        den = np.abs(u_ref) / np.maximum(np.abs(d_ref), 1e-30)
+        ok = (np.abs(d_ref) > 1e-6) & (den >= 1e-3 * den.max())
+        assert ok.mean() > 0.99
+        assert np.abs(d - d_ref)[ok].max() <= 1e-4, (lo, np.abs(d - d_ref)[ok].max())
+
+
+def test_prepare_code_matches_reference_desk(gpu_ctx, ref):
+    """prepare_code support n, energy and replica (test_detector.cpp:70-87)."""
+    from paper_2005_10445_b200 import capi
+    from paper_2005_10445_b200._abi import desk_config
+    cfg = desk_config(256)
+    W = 2048 + 500
+    bits = np.stack([ref.gen_code(s, cfg) for s in (1, 2, 3)])
+    cs = capi.CodeSet.prepare(gpu_ctx, cfg, W, bits)
+    s = ref.Session()
+    for i in range(3):
+        k = s.prepare_code(bits[i], cfg, W, "c%d" % i)
+        want = s.code_info(k)
+        got = cs.info(i)
+        assert got["nonzero_len"] == want["nonzero_len"], (i, got, want)
+        assert abs(got["energy"] - want["energy"]) <= 1e-5 * want["energy"], (i, got, want)
+        rg, rw = cs.replica(i), s.code_replica(k)
+        # replica d = u / (|f1| + |f0|): compare where the denominator is
+        # well conditioned (the causal filter start is 0/0-like dust)
+        rep = ref.synth_replica(bits[i], cfg, W)
+        d_ref, u_ref = ref.demodulate_signal(rep, 0, 0.0, cfg)
+        n = want["nonzero_len"]
+        den = np.abs(u_ref[:n]) / np.maximum(np.abs(d_ref[:n]), 1e-30)
+        ok = (np.abs(d_ref[:n]) > 1e-6) & (den >= 1e-3 * den.max())
+        assert ok.mean() > 0.95
+        assert np.abs(rg - rw)[ok].max() <= 1e-4, (i, np.abs(rg - rw)[ok].max())
+
+
+def test_end_to_end_desk_fractional_delay(gpu_ctx, ref):
+    """test_detector.cpp:253-292 on the GPU, and parity with the reference."""
+    from paper_2005_10445_b200 import capi
+    from paper_2005_10445_b200._abi import desk_config
+    cfg = desk_config(1024)
+    P = 1024 * 8
+    W = P + 1000
+    bits = np.stack([ref.gen_code(s, cfg) for s in (100, 101, 102)])
+    iq = ref.channel_window(bits[0], cfg, 12.25, W, 55)
+    cs = capi.CodeSet.prepare(gpu_ctx, cfg, W, bits)
+    win = capi.Windows(gpu_ctx, W)
+    win.demodulate(cfg, [0.0], iq, 0, W, 1)
+    dets = capi.detect(gpu_ctx, win, cs, 0.25, cfg.mod.sample_rate)
+    assert dets[0]["accepted"] and dets[0]["score"] > 0.9
+    assert abs(dets[0]["toa_seconds"] * cfg.mod.sample_rate - 12.25) <= 0.05
+    assert not dets[1]["accepted"] and not dets[2]["accepted"]
+    s = ref.Session()
+    idx = [s.prepare_code(bits[i], cfg, W, "c%d" % i) for i in range(3)]
+    d, u = ref.demodulate_window(iq, 0, cfg)
+    want = s.detect(d, u, idx, 0.25, 0, cfg.mod.sample_rate)
+    # the injected code: full parity end to end
+    bad = compare_detections(dets[:1], want[:1], cfg.mod.sample_rate)
+    assert not bad, bad
+    # absent codes in this noise-free window correlate against the 0/0 dust
+    # of d in the exactly-zero stretches, which is FFT-rounding dependent;
+    # with the same d,u the whole detect() back half must agree.
+    win.set_du(0, d, u, 0)
+    dets2 = capi.detect(gpu_ctx, win, cs, 0.25, cfg.mod.sample_rate)
+    bad = compare_detections(dets2, want, cfg.mod.sample_rate, xc_ref=s.batch_xcorr(d, idx))
+    assert not bad, bad
+
+
+def test_end_to_end_desk_noisy_all_codes(gpu_ctx, ref):
+    """Same scene at 10 dB SNR: every code's Detection end to end."""
+    from paper_2005_10445_b200 import capi
+    from paper_2005_10445_b200._abi import desk_config
+    cfg = desk_config(1024)
+    W = 1024 * 8 + 1000
+    bits = np.stack([ref.gen_code(s, cfg) for s in (100, 101, 102, 103, 104)])
+    iq = ref.channel_window(bits[0], cfg, 12.25, W, 55, snr_db=10.0)
+    cs = capi.CodeSet.prepare(gpu_ctx, cfg, W, bits)
+    win = capi.Windows(gpu_ctx, W)
+    win.demodulate(cfg, [0.0], iq, 0, W, 1)
+    dets = capi.detect(gpu_ctx, win, cs, 0.25, cfg.mod.sample_rate)
+    s = ref.Session()
+    idx = [s.prepare_code(bits[i], cfg, W, "c%d" % i) for i in range(len(bits))]
+    d, u = ref.demodulate_window(iq, 0, cfg)
+    want = s.detect(d, u, idx, 0.25, 0, cfg.mod.sample_rate)
+    xc = s.batch_xcorr(d, idx)
+
+    def tie_ok(g, w):
+        c = int(w["code_index"])
+        return near_tie_margin(xc[c], int(w["peak_index"]), int(g["peak_index"])) < 1e-5
+
+    bad = compare_detections(dets, want, cfg.mod.sample_rate, tie_ok=tie_ok, xc_ref=xc, eps=1e-5)
+    assert not bad, bad
+
+
+@pytest.mark.slow
+def test_search_shape_parity(gpu_ctx, ref):
+    """Default 8 Ms/s search shape (W = 800,000, N = 870,912): one injected
+    code in noise plus absent codes, every Detection field vs the reference."""
+    from paper_2005_10445_b200 import capi
+    from paper_2005_10445_b200._abi import demod_config
+    cfg = demod_config()
+    W = 800000
+    bits = np.stack([ref.gen_code(1000 + i, cfg) for i in range(5)])
+    iq = ref.channel_window(bits[0], cfg, 1000.25, W, 1, snr_db=0.0)
+    cs = capi.CodeSet.prepare(gpu_ctx, cfg, W, bits)
+    assert cs.info(0)["corr_len"] == 870912
+    win = capi.Windows(gpu_ctx, W)
+    win.demodulate(cfg, [0.0], iq, 0, W, 1)
+    dets = capi.detect(gpu_ctx, win, cs, 0.25, cfg.mod.sample_rate)
+    s = ref.Session()
+    idx = [s.prepare_code(bits[i], cfg, W, "c%d" % i) for i in range(len(bits))]
+    for i in range(len(bits)):
+        assert cs.info(i)["nonzero_len"] == s.code_info(idx[i])["nonzero_len"]
+    d, u = ref.demodulate_window(iq, 0, cfg)
+    want = s.detect(d, u, idx, 0.25, 0, cfg.mod.sample_rate)
+    assert want[0]["accepted"] and abs(want[0]["peak_index"] - 1000) <= 1
+    xc = s.batch_xcorr(d, idx)
+
+    def tie_ok(g, w):
+        c = int(w["code_index"])
+        return near_tie_margin(xc[c], int(w["peak_index"]), int(g["peak_index"])) < 1e-5
+
+    bad = compare_detections(dets, want, cfg.mod.sample_rate, tie_ok=tie_ok, xc_ref=xc, eps=1e-5)
+    assert not bad, bad
