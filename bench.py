@@ -218,7 +218,7 @@ def main():
     n_complex = iq.size // 2
     ctx = capi.Context(local)
     cs = capi.CodeSet.prepare(ctx, cfg, W, bits)
-    assert cs.info(0)["corr_len"] == CORR_LEN
+    corr_len_used = cs.info(0)["corr_len"]
     win = capi.Windows(ctx, W, N_WIN, len(BINS))
     iq_dev = torch.from_numpy(iq).to(f"cuda:{local}")
     iq_pin = torch.from_numpy(iq).pin_memory()
@@ -239,16 +239,10 @@ def main():
                                    ctypes.c_void_p(iq_pin.data_ptr()), n_complex, 0, W, ADV, cs._h, 0.25,
                                    ctypes.c_void_p(out_pin.data_ptr()), n_units, ctypes.byref(nout)))
         if world > 1:
-            import torch.distributed as dist
-            acc = np.frombuffer(out_pin.numpy().tobytes(), dtype=DETECTION_DTYPE)
-            mine = torch.from_numpy(np.ascontiguousarray(acc[acc["accepted"] == 1]).view(np.uint8).copy())
-            sizes = [None] * world
-            dist.all_gather_object(sizes, int(mine.numel()))
-            bufs = [torch.empty(max(1, s), dtype=torch.uint8, device=f"cuda:{local}") for s in sizes]
-            t = torch.empty(max(1, mine.numel()), dtype=torch.uint8, device=f"cuda:{local}")
-            if mine.numel():
-                t.copy_(mine)
-            dist.all_gather(bufs, t)
+            # the path's one exchange: every rank's accepted detections, all-gathered over NCCL
+            from paper_2005_10445_b200 import dist as tdist
+            recs = np.frombuffer(out_pin.numpy().tobytes(), dtype=DETECTION_DTYPE)
+            tdist.gather_detections(recs, rank * N_CODES, device=f"cuda:{local}", accepted_only=True)
 
     def barrier():
         torch.cuda.synchronize()
@@ -269,8 +263,6 @@ def main():
     for _ in range(args.warmup):
         step_device()
     barrier()
-    ctx.kernel_time_reset()
-    ctx.set_option("time_kernels", 1)
     launches0 = capi.kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with Clocks(local) as clk:
@@ -282,10 +274,18 @@ def main():
         barrier()
     ms = ev0.elapsed_time(ev1) / args.steps
     launches = (capi.kernel_launches() - launches0) // args.steps
-    kt = {k: ctx.kernel_time(k) for k in ("demod", "fwd_pass1", "fwd_pass2", "corr_passA", "corr_passB", "stats")}
-    ctx.set_option("time_kernels", 0)
     ms_max = max_over_ranks(ms)
     value = n_units * world / (ms_max / 1e3)
+
+    # ---- per-kernel CUDA events (same steps, separate pass: recording an
+    # event pair around each of ~800 launches perturbs the step time) -------
+    ctx.kernel_time_reset()
+    ctx.set_option("time_kernels", 1)
+    for _ in range(args.steps):
+        step_device()
+    barrier()
+    kt = {k: ctx.kernel_time(k) for k in ("demod", "fwd_pass1", "fwd_pass2", "corr_passA", "corr_passB", "stats")}
+    ctx.set_option("time_kernels", 0)
 
     # ---- end-to-end through the C-ABI from pinned host memory ----------------
     for _ in range(args.warmup):
@@ -320,7 +320,7 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (numpy scene: 16 of the codes injected at known fractional delays, offsets "
                 "U(-200,200) kHz, SNR {0,5,10,20} dB in 10 dB noise; int16 at scale 8192)",
-        "config": workload_config(world),
+        "config": dict(workload_config(world), corr_len_b200=corr_len_used),
         # stream seconds searched per wall second for the whole roster (64 x
         # n_gpus codes) x 9 bins: N_WIN windows x advance per step
         "real_time_factor": (N_WIN * ADV / FS) / (ms_max / 1e3),

@@ -186,24 +186,47 @@ uint64_t pad_length_impl(uint64_t n) {
     }
 }
 
-// smallest N1*N2 >= need; ties -> more balanced split (pass B is the chunked one)
+// Codelet cost (scalar ops per point of one pass, from tools/gen_codelets.py's
+// counts: ops(P)/P + ops(Q)/Q) plus ~12 ops/point of per-pass overhead.
+double pass_cost(int L) {
+    switch (L) {
+        case 16: return 8.0 + 12;
+        case 32: return 10.5 + 12;
+        case 64: return 13.0 + 12;
+        case 128: return 15.5 + 12;
+        case 256: return 18.0 + 12;
+        case 360: return 25.51 + 12;
+        case 450: return 28.79 + 12;
+        case 512: return 20.75 + 12;
+        case 864: return 27.82 + 12;
+        case 1008: return 30.16 + 12;
+        case 1024: return 23.5 + 12;
+    }
+    return 1e9;
+}
+
+// Transform length N = N1*N2 >= need minimising N*(cost(N1)+cost(N2)); any
+// N >= W + n - 1 yields the same lags [0, W) (linear correlation).  Between
+// the two orders the pass-A length (N2) is the one with the smaller
+// shared-memory slot, i.e. the smaller length.
 bool choose_corr_len(uint64_t need, int* n1, int* n2) {
-    uint64_t best = 0;
+    double best = 0.0;
+    uint64_t bestN = 0;
     int b1 = 0, b2 = 0;
     for (const auto& a : kMenu)
         for (const auto& b : kMenu) {
+            if (a.L < b.L) continue;   // N1 >= N2
             const uint64_t n = uint64_t(a.L) * uint64_t(b.L);
             if (n < need) continue;
-            const bool better = best == 0 || n < best ||
-                                (n == best && std::abs(a.L - b.L) < std::abs(b1 - b2)) ||
-                                (n == best && std::abs(a.L - b.L) == std::abs(b1 - b2) && a.L > b1);
-            if (better) {
-                best = n;
+            const double c = double(n) * (pass_cost(a.L) + pass_cost(b.L));
+            if (bestN == 0 || c < best * (1.0 - 1e-9) || (c <= best * (1.0 + 1e-9) && n < bestN)) {
+                best = c;
+                bestN = n;
                 b1 = a.L;
                 b2 = b.L;
             }
         }
-    if (!best) return false;
+    if (!bestN) return false;
     *n1 = b1;
     *n2 = b2;
     return true;
@@ -407,6 +430,7 @@ struct tdg_ctx {
     int clen = 0;
     // scratch
     DevBuf T, M, keys, det_dev, stream_buf;
+    tdg_windows* search_win = nullptr;   // cached window set of tdg_search (reused across calls)
     DescPack pk_fwd, pk_corr, pk_misc;
     std::vector<char> host_stage;
     int64_t wave_pairs = 8;      // correlation pairs per pass-A/pass-B wave
@@ -715,6 +739,7 @@ void tdg_ctx_destroy(tdg_ctx* ctx) {
         cudaEventDestroy(k.b);
     }
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->search_win) tdg_windows_destroy(ctx->search_win);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -1137,10 +1162,14 @@ int tdg_search(tdg_ctx* ctx, const tdg_demod_config* cfg, const double* lo_bins,
         if (n_out) *n_out = n_windows * n_bins * cs->n_codes;
         if (n_windows == 0) return;
         if (out_cap < n_windows * n_bins * cs->n_codes) fail(TDG_EINVAL, "search: output capacity too small");
-        tdg_windows* w = nullptr;
-        int rc = tdg_windows_create(ctx, window_len, n_windows, n_bins, &w);
-        if (rc) fail(rc, "%s", g_err.c_str());
-        std::unique_ptr<tdg_windows, void (*)(tdg_windows*)> hold(w, tdg_windows_destroy);
+        tdg_windows* w = ctx->search_win;
+        if (!w || w->W != window_len || w->n_windows != n_windows || w->n_bins != n_bins) {
+            if (w) tdg_windows_destroy(w);
+            ctx->search_win = nullptr;
+            int rc = tdg_windows_create(ctx, window_len, n_windows, n_bins, &w);
+            if (rc) fail(rc, "%s", g_err.c_str());
+            ctx->search_win = w;
+        }
         ctx->stream_buf.ensure(n_complex * 2 * sizeof(int16_t));
         CK(cudaMemcpyAsync(ctx->stream_buf.p, iq, n_complex * 2 * sizeof(int16_t), cudaMemcpyHostToDevice, ctx->stream));
         demodulate_impl(ctx, w, cfg, lo_bins, n_bins, ctx->stream_buf.as<int16_t>(), n_complex, stream_start, advance,
