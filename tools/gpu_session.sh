@@ -1,0 +1,32 @@
+#!/bin/bash
+# One gpurun session: GPU parity tests, smoke, bench, launch list, ncu capture
+# of the two correlation passes.  Usage (from the repo root, on the GPU box):
+#   bash tools/gpu_session.sh [tag] [what...]   what: tests smoke bench launches ncu
+set -x
+TAG=${1:-run}; shift
+WHAT=${@:-tests smoke bench launches ncu}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.limit --format=csv > $OUT/gpu.txt 2>&1
+lscpu > $OUT/lscpu.txt 2>&1
+for w in $WHAT; do
+case $w in
+tests)
+  timeout 900 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log ;;
+smoke)
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log ;;
+bench)
+  timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err ;;
+benchfast)
+  timeout 600 python bench.py --no-cpu-baseline > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err ;;
+launches)
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 1000 -c 1200 --csv \
+      --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/launches_bench.log 2>&1 ;;
+ncu)
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_corr_passA2 -s 40 -c 1 \
+      -o $OUT/passA python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncuA.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_corr_passB2 -s 40 -c 1 \
+      -o $OUT/passB python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncuB.log 2>&1 ;;
+esac
+done
+ls -la $OUT
