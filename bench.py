@@ -54,7 +54,7 @@ def bytes_per_corr(n_bins, n_codes):
 
 
 def peaks():
-    p = {"hbm_gbs": 6559.7, "source": "fallback (B200_PROFILING.md)"}
+    p = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md: 6.65 TB/s)"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             m = json.load(f)
@@ -66,28 +66,39 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi sampling (B200_PROFILING.md clocks line).  The sampler is
+    started before the warm-up (nvidia-smi needs ~0.1-0.3 s to produce its
+    first sample) and only the samples whose timestamps fall inside the
+    timed region (mark_start/mark_end, host clock) are summarised."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.t0 = self.t1 = None
+        self.lines = []
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.Q, "--format=csv,noheader,nounits",
-                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                          "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
                                          text=True)
         except Exception:
             self.proc = None
         return self
 
-    def __exit__(self, *a):
-        self.lines = []
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
+
+    def stop(self):
         if self.proc:
+            time.sleep(0.06)
             self.proc.terminate()
             try:
                 out, _ = self.proc.communicate(timeout=5)
@@ -95,24 +106,32 @@ class Clocks:
                 self.proc.kill()
                 out, _ = self.proc.communicate()
             self.lines = [l for l in out.splitlines() if l.strip()]
+            self.proc = None
 
     def summary(self):
+        import datetime
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
+        for l in self.lines:
             f = [x.strip() for x in l.split(",")]
-            if len(f) < 9 or f[0] != str(self.index):
+            if len(f) < 10 or f[1] != str(self.index):
                 continue
             try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
             except ValueError:
                 continue
-            for nm, v in zip(names, f[5:9]):
+            if self.t0 is not None and not (self.t0 - 0.025 <= ts <= self.t1 + 0.025):
+                continue
+            try:
+                sm.append(float(f[2]))
+                mx = float(f[3])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[6:10]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "window_s": (self.t1 - self.t0) if self.t0 is not None else None}
 
 
 def dist_env():
@@ -191,11 +210,13 @@ def cpu_baseline_sample(bits, iq):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--ref-codes", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-step", action="store_true",
+                    help="run one extra device step between cudaProfilerStart/Stop (ncu --profile-from-start off)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     if args.impl == "reference":
@@ -260,22 +281,31 @@ def main():
         return float(t.item())
 
     # ---- device-resident timed region ---------------------------------------
+    clk = Clocks(local).start()
     for _ in range(args.warmup):
         step_device()
     barrier()
     launches0 = capi.kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with Clocks(local) as clk:
-        barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step_device()
-        ev1.record(stream)
-        barrier()
+    barrier()
+    clk.mark_start()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step_device()
+    ev1.record(stream)
+    barrier()
+    clk.mark_end()
+    clk.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     launches = (capi.kernel_launches() - launches0) // args.steps
     ms_max = max_over_ranks(ms)
     value = n_units * world / (ms_max / 1e3)
+
+    if args.profile_step:
+        torch.cuda.cudart().cudaProfilerStart()
+        step_device()
+        barrier()
+        torch.cuda.cudart().cudaProfilerStop()
 
     # ---- per-kernel CUDA events (same steps, separate pass: recording an
     # event pair around each of ~800 launches perturbs the step time) -------
@@ -284,7 +314,7 @@ def main():
     for _ in range(args.steps):
         step_device()
     barrier()
-    kt = {k: ctx.kernel_time(k) for k in ("demod", "fwd_pass1", "fwd_pass2", "corr_passA", "corr_passB", "stats")}
+    kt = {k: ctx.kernel_time(k) for k in ("demod", "fwd_pass1", "fwd_pass2", "corr", "stats")}
     ctx.set_option("time_kernels", 0)
 
     # ---- end-to-end through the C-ABI from pinned host memory ----------------
@@ -301,15 +331,22 @@ def main():
     wall_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / args.steps)
     e2e = n_units * world / (e2e_ms / 1e3)
 
-    # ---- roofline of the dominant kernel (pass A) ---------------------------
+    # ---- roofline of the dominant stage: the correlation engine -------------
+    # (k_corr_pass pass A + pass B on two streams, one per-step event pair)
     pk = peaks()
-    nA, msA = kt["corr_passA"]
-    per_launch_ms = msA / max(1, nA)
-    corr_per_launch = n_units / max(1, nA / args.steps)
+    n_corr_launch, ms_corr = kt["corr"]
+    corr_ms_step = ms_corr / max(1, n_corr_launch)
     bpc = bytes_per_corr(len(BINS), N_CODES)
-    achieved = bpc * corr_per_launch / (per_launch_ms / 1e3) / 1e9
+    achieved = bpc * n_units / (corr_ms_step / 1e3) / 1e9
     total_ms = sum(v[1] for v in kt.values())
     shares = {k: round(v[1] / total_ms, 4) if total_ms else None for k, v in kt.items()}
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        traffic = tj["corr_dram_bytes_per_step"]
+    except Exception:
+        pass
 
     if rank != 0:
         return
@@ -329,13 +366,18 @@ def main():
                 "h2d_bytes_per_step": int(iq.nbytes), "d2h_bytes_per_step": int(n_units * DETECTION_DTYPE.itemsize),
                 "path": "tdg_search() C-ABI, pinned host int16 in, Detection records out"},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm", "kernel": "k_corr_passA2 (fused spectral product + first inverse-FFT pass)",
+        "roofline": {"bound": "hbm",
+                     "kernel": "correlation engine per step: k_corr_pass<27,32,32,32,0> (spectral product + "
+                               "first inverse-FFT pass) and k_corr_pass<...,1> (second pass + argmax), "
+                               "%d launches on two overlapped streams" % (2 * ((N_CODES // 2 + 7) // 8) * N_WIN * len(BINS)),
                      "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
-                     "traffic": None, "peak_source": pk["source"],
-                     "algorithmic_bytes_per_corr": bpc,
-                     "corr_per_launch": corr_per_launch, "avg_launch_ms": per_launch_ms,
-                     "fp32": {"achieved_tflops": value / world * FLOP_CORR / 1e12,
-                              "note": "SURVEY 8(d) 47.6 MFLOP/correlation, whole step"}},
+                     "traffic": traffic, "peak_source": pk["source"],
+                     "traffic_note": "dram__bytes_read+write of all correlation launches of one step, warm L2 "
+                                     "(ncu --cache-control none, profiles/traffic.json)",
+                     "algorithmic_bytes_per_corr": bpc, "corr_per_step": n_units, "stage_ms_per_step": corr_ms_step,
+                     "fp32": {"achieved_tflops": n_units * FLOP_CORR / (corr_ms_step / 1e3) / 1e12,
+                              "note": "SURVEY 8(d) 47.6 MFLOP/correlation over the correlation stage; the "
+                                      "stage is FP32-issue bound, not HBM bound (DESIGN.md section 4)"}},
         "kernel_ms_per_step": {k: v[1] / args.steps for k, v in kt.items()},
         "kernel_share": shares,
         "clocks": clk.summary(),

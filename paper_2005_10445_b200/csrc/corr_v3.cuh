@@ -1,0 +1,371 @@
+// Correlation engine v3: the two inverse-FFT passes of every (window slot x
+// code pair) correlation as two persistent, TMA-pipelined kernels per wave
+// of `wave_pairs` pairs, issued on two CUDA streams so that pass B of wave w
+// overlaps pass A of wave w+1 (no SM idles in a launch's ramp or tail):
+//
+//   correlate_spectrum (proj/src/detector.cpp:78-88)  ->  pass A
+//   inverse FFT + find_peak (detector.cpp:122-134)     ->  pass A + pass B
+//
+// Pass-A items: column pair cp x group of <= kGroup code pairs sharing one
+// window spectrum.  Pass-B items: pair x tile of kTileB t2 columns of the
+// inter-pass intermediate M, which lives in a ring of `ring` wave buffers
+// (events order A(w) after B(w-ring)).  Jobs are ordered code-pair-major so
+// a group's code spectra stay L2-resident (evict_last) while the window
+// spectra stream through (evict_first), and pass B drops each M tile from L2
+// after reading it (discard: no DRAM write-back of dead data).
+//
+// Inside a CTA, thread 0 prefetches the next item's operands with 1-D bulk
+// copies (cp.async.bulk -> UBLKCP, completing on an mbarrier) into the
+// second shared-memory slot while the 4 warps run the current item from the
+// first.  Pass-A inter-pass twiddles come from a precomputed table that rides
+// in the same bulk copies, so no item recomputes sincos.
+#pragma once
+#include "kernels.cuh"
+#include "tma.cuh"
+
+namespace tdg {
+
+constexpr int kTileB = 4;   // t2 columns per pass-B tile (M is stored tile-major)
+constexpr int kGroup = 2;   // code pairs per pass-A item (sharing one window spectrum column)
+
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+__host__ __device__ constexpr int qstride_even_pad(int q) { return (q % 2) ? q : q + 1; }
+// pass-B transposed row stride (float2 units): == 4 or 12 (mod 16) so that a
+// half-warp of 4 a-values x 4 t2-columns hits 16 distinct 8-byte bank pairs
+__host__ __device__ constexpr int passb_row(int q) {
+    return ((q * kTileB) % 16 == 4 || (q * kTileB) % 16 == 12) ? q * kTileB
+           : ((q * kTileB) % 16 == 0) ? q * kTileB + 4
+                                      : q * kTileB + 12 - ((q * kTileB) % 16) + ((q * kTileB) % 16 > 12 ? 16 : 0);
+}
+__host__ __device__ constexpr int even_up(int x) { return (x + 1) & ~1; }
+
+// Inter-pass twiddle table row stride (float2): row k1 holds
+// [w_N^{+k1 c}, c < QA][w_N^{+k1 QA e}, e < PA], padded to a 16-byte multiple.
+__host__ __device__ constexpr int inter_tw_stride(int PA, int QA) { return even_up(PA + QA); }
+
+template <int PA, int QA, int PB, int QB>
+struct Fused {
+    static constexpr int LA = PA * QA, LB = PB * QB;
+    static constexpr int QSA = qstride_even_pad(QA);
+    static constexpr int TWS = inter_tw_stride(PA, QA);
+    // pass-A slot: [D column][X columns: 2 per pair][transpose reuses D/X] [2 twiddle rows]
+    static constexpr int A_OPS = even_up(cmax((1 + 2 * kGroup) * LA, kGroup * 2 * PA * QSA));
+    static constexpr int A_SLOT = A_OPS + 2 * TWS;
+    static constexpr int ROWB = passb_row(QB);
+    static constexpr int B_SLOT = even_up(cmax(LB * kTileB, PB * ROWB));
+    static constexpr int SLOT = cmax(A_SLOT, B_SLOT);
+    static constexpr int NT = 128;
+    static constexpr size_t SMEM = 128 + 2 * size_t(SLOT) * 8;
+    static_assert(cmax(PA, QA) <= 32 && cmax(PB, QB) <= 32, "one warp per column role");
+    static_assert(kTileB * cmax(PB, QB) <= NT, "pass-B tasks fit the CTA");
+};
+
+struct CorrSched {                     // one wave
+    const CorrGroup<kGroup>* groups;   // [ngw]
+    const CorrPairOut* outs;           // [wave_pairs]
+    const float2* twA;                 // w_{N2}^{+ac}, index a*QA + c
+    const float2* twB;                 // w_{N1}^{+ac}, index a*QB + c
+    const float2* twI;                 // inter-pass rows, stride inter_tw_stride
+    int ngw, wave_pairs, n_tiles, nA, nB, N1, N2;
+    int write_xc;                      // 1: full xc rows (batch_xcorr), 0: argmax keys
+    int discard;                       // 1: drop consumed M tiles from L2 (no write-back)
+    uint32_t W;
+    float inv_n;
+};
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// threadIdx.x through a volatile read: the item bodies recompute their
+// lane-dependent addresses per item instead of letting NVVM hoist them out of
+// the persistent loop, where pass A's and pass B's invariants together would
+// stay live across both bodies and spill.
+__device__ __forceinline__ int tid_x() {
+    int t;
+    asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
+    return t;
+}
+
+struct Ticket {
+    int type;   // 0 = pass A, 1 = pass B
+    int w;
+    int idx;
+};
+
+__device__ __forceinline__ bool ticket_noop(const CorrSched& S, const Ticket& k) {
+    if (k.type == 0) return S.groups[k.idx % S.ngw].npairs == 0;
+    return S.outs[k.idx / S.n_tiles].M == nullptr;
+}
+
+// thread 0: bulk copies of a (non-noop, ready) item into slot sl
+template <int PA, int QA, int PB, int QB>
+__device__ __forceinline__ void issue_ticket(const CorrSched& S, const Ticket& k, float2* sl, uint64_t* bar) {
+    using F = Fused<PA, QA, PB, QB>;
+    fence_proxy_async_smem();     // earlier generic use of this slot before the async writes
+    fence_proxy_async_global();   // M written by other CTAs (acquired) before the async reads
+    if (k.type == 0) {
+        constexpr int LA = F::LA, TWS = F::TWS;
+        const int cp = k.idx / S.ngw;
+        const CorrGroup<kGroup>& gd = S.groups[k.idx % S.ngw];
+        const bool self = (cp == 0) || (2 * cp == F::LB);
+        const uint32_t bytes = uint32_t(LA) * 8u * uint32_t(1 + gd.npairs * (self ? 1 : 2)) + 2u * TWS * 8u;
+        mbar_arrive_expect_tx(bar, bytes);
+        // window spectrum: read by this wave only; code spectra: reused by
+        // the next waves (jobs are ordered code-pair-major)
+        const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+        bulk_g2s_hint(sl, gd.D + size_t(cp) * LA, LA * 8, bar, pol_first);
+        for (int g = 0; g < gd.npairs; ++g) {
+            const float2* X = gd.Ca[g];
+            bulk_g2s_hint(sl + (1 + 2 * g) * LA, X + size_t(self ? cp : F::LB - cp) * LA, LA * 8, bar, pol_last);
+            if (!self) bulk_g2s_hint(sl + (2 + 2 * g) * LA, X + size_t(cp) * LA, LA * 8, bar, pol_last);
+        }
+        const int k1b = cp == 0 ? 0 : F::LB - cp;
+        bulk_g2s(sl + F::A_OPS, S.twI + size_t(cp) * TWS, TWS * 8, bar);
+        bulk_g2s(sl + F::A_OPS + TWS, S.twI + size_t(k1b) * TWS, TWS * 8, bar);
+    } else {
+        constexpr int LB = F::LB;
+        const CorrPairOut& po = S.outs[k.idx / S.n_tiles];
+        const int tb = k.idx % S.n_tiles;
+        mbar_arrive_expect_tx(bar, LB * kTileB * 8);
+        bulk_g2s_hint(sl, po.M + size_t(tb) * LB * kTileB, LB * kTileB * 8, bar, policy_evict_first());
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Pass A item: column pair (cp, N1-cp) x up to kGroup code pairs of one
+// window.  Code pairs are stored as the full spectrum X = FFT(dc_a + i dc_b)
+// in column layout, so with the window's Hermitian half-column D:
+//   Z[k]   = D[k] (conj Ca[k] + i conj Cb[k]) = D[k] X[N-k]
+//   Z[N-k] = conj(D[k]) (Ca[k] + i Cb[k])     = conj(D[k]) X[k]
+// i.e. one complex multiply per point; IFFT(Z) = xc_a + i xc_b.  Output: M,
+// tile-major M[(t2/kTileB)*N1*kTileB + k1*kTileB + t2%kTileB], times the
+// inter-pass twiddle w_N^{+k1 t2}.
+template <int PA, int QA, int PB, int QB>
+__device__ __forceinline__ void item_passA(const CorrSched& S, const Ticket& k, float2* sl) {
+    using F = Fused<PA, QA, PB, QB>;
+    constexpr int P = PA, Q = QA, L = F::LA, QS = F::QSA, TWS = F::TWS;
+    constexpr int N1 = F::LB;   // pass-B length == number of columns
+    const int cp = k.idx / S.ngw;
+    const int tid = tid_x();
+    const CorrGroup<kGroup>& gd = S.groups[k.idx % S.ngw];
+    const int npairs = gd.npairs;
+    const bool self = (cp == 0) || (2 * cp == N1);
+    const int role = tid >> 5;   // warp-uniform (g, col)
+    const int g = role >> 1, col = role & 1;
+    const int lane = tid & 31;
+    const bool act = g < npairs && (col == 0 || !self);
+    // ---- step 1: lane a: product + Q-point IDFT over rows r = a + P*b
+    float2 v[Q];
+    const bool act1 = act && lane < P;
+    if (act1) {
+        const int a = lane;
+        const float2* D = sl;
+        const float2* Xm = sl + (1 + 2 * g) * L;   // X column N1-cp (or cp if self)
+        if (col == 0) {
+            if (cp == 0) {
+#pragma unroll
+                for (int b = 0; b < Q; ++b) {
+                    const int r = a + P * b;
+                    v[b] = cmul(D[r], Xm[r == 0 ? 0 : L - r]);
+                }
+            } else {
+#pragma unroll
+                for (int b = 0; b < Q; ++b) {
+                    const int r = a + P * b;
+                    v[b] = cmul(D[r], Xm[L - 1 - r]);
+                }
+            }
+        } else {
+            const float2* Xc = sl + (2 + 2 * g) * L;  // X column cp
+#pragma unroll
+            for (int b = 0; b < Q; ++b) {
+                const int r = (L - 1) - (a + P * b);   // source row of output row a + P*b
+                v[b] = cmulc(Xc[r], D[r]);
+            }
+        }
+        dft<Q, +1>(v);
+    }
+    __syncthreads();  // operands consumed
+    if (act1) {
+        float2* tr = sl + role * P * QS + lane * QS;
+#pragma unroll
+        for (int c = 0; c < Q; ++c) tr[c] = v[c];
+    }
+    __syncthreads();
+    // ---- step 2: lane c: twiddle, P-point IDFT over a, inter-pass twiddle, store M
+    if (act && lane < Q) {
+        const int c = lane;
+        const float2* tr = sl + role * P * QS + c;
+        float2 w[P];
+#pragma unroll
+        for (int a = 0; a < P; ++a) {
+            const float2 x = tr[a * QS];
+            w[a] = a == 0 ? x : cmul(x, __ldg(&S.twA[a * Q + c]));
+        }
+        dft<P, +1>(w);
+        const int k1 = col ? N1 - cp : cp;
+        const float2* twr = sl + F::A_OPS + col * TWS;
+        const float2 tc = twr[c];
+        float2* M = gd.M[g] + size_t(k1) * kTileB + (c % kTileB) + size_t(c / kTileB) * N1 * kTileB;
+#pragma unroll
+        for (int e = 0; e < P; ++e) {
+            const int t2 = c + Q * e;
+            const float2 tt = cmul(tc, twr[Q + e]);
+            if (Q % kTileB == 0)
+                M[size_t(Q / kTileB) * e * N1 * kTileB] = cmul(w[e], tt);
+            else
+                gd.M[g][(size_t(t2 / kTileB) * N1 + k1) * kTileB + (t2 % kTileB)] = cmul(w[e], tt);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Pass B item: (pair, tile of kTileB t2 columns); tile = N1 x kTileB
+// contiguous float2 of M.  y[t2 + N2*t1] = xc_a + i*xc_b (times N).
+// Epilogue: first-index argmax of |Re|, |Im| over lags t < W (find_peak,
+// proj/src/detector.cpp:122-134) merged with atomicMax on packed keys, or
+// the full xc rows (batch_xcorr diagnostics).
+template <int PA, int QA, int PB, int QB>
+__device__ __forceinline__ void item_passB(const CorrSched& S, const Ticket& k, float2* sl) {
+    using F = Fused<PA, QA, PB, QB>;
+    constexpr int P = PB, Q = QB, ROW = F::ROWB, TB = kTileB;
+    const CorrPairOut& po = S.outs[k.idx / S.n_tiles];
+    const int tb = k.idx % S.n_tiles;
+    const int tid = tid_x();
+    constexpr int N2 = F::LA;   // pass-A length == number of t2 columns
+    const uint32_t W = S.W;
+    // step 1: task (a, t2l), t2l fastest
+    const int t2l1 = tid % TB, a1 = tid / TB;
+    const bool act1 = a1 < P;
+    float2 v[Q];
+    if (act1) {
+#pragma unroll
+        for (int b = 0; b < Q; ++b) v[b] = sl[(a1 + P * b) * TB + t2l1];
+        dft<Q, +1>(v);
+    }
+    __syncthreads();
+    if (act1) {
+#pragma unroll
+        for (int c = 0; c < Q; ++c) sl[a1 * ROW + c * TB + t2l1] = v[c];
+    }
+    __syncthreads();
+    // step 2: task (c, t2l)
+    const int t2l = tid % TB, c = tid / TB;
+    const int t2 = tb * TB + t2l;
+    float best_a = -1.f, best_b = -1.f;
+    uint32_t idx_a = 0, idx_b = 0;
+    if (c < Q) {
+        float2 w[P];
+#pragma unroll
+        for (int a = 0; a < P; ++a) {
+            const float2 x = sl[a * ROW + c * TB + t2l];
+            w[a] = a == 0 ? x : cmul(x, __ldg(&S.twB[a * Q + c]));
+        }
+        dft<P, +1>(w);
+        // valid lags t = t2 + N2*(c + Q*e) < W form a prefix e < e_lim
+        int e_lim = 0;
+        if (t2 < N2 && uint32_t(t2) < W) {
+            const int t1max = int((W - 1u - uint32_t(t2)) / uint32_t(N2));
+            e_lim = t1max >= c ? (t1max - c) / Q + 1 : 0;
+            e_lim = e_lim < P ? e_lim : P;
+        }
+        if (S.write_xc) {
+#pragma unroll
+            for (int e = 0; e < P; ++e) {
+                if (e < e_lim) {
+                    const uint32_t t = uint32_t(t2) + uint32_t(N2) * uint32_t(c + Q * e);
+                    if (po.xc_a) po.xc_a[t] = w[e].x * S.inv_n;
+                    if (po.xc_b) po.xc_b[t] = w[e].y * S.inv_n;
+                }
+            }
+        } else if (e_lim > 0) {
+            // t increases with e: strict '>' keeps the first index
+            int ea = 0, eb = 0;
+#pragma unroll
+            for (int e = 0; e < P; ++e) {
+                if (e < e_lim) {
+                    const float ma = fabsf(w[e].x), mb = fabsf(w[e].y);
+                    if (ma > best_a) {
+                        best_a = ma;
+                        ea = e;
+                    }
+                    if (mb > best_b) {
+                        best_b = mb;
+                        eb = e;
+                    }
+                }
+            }
+            idx_a = uint32_t(t2) + uint32_t(N2) * uint32_t(c + Q * ea);
+            idx_b = uint32_t(t2) + uint32_t(N2) * uint32_t(c + Q * eb);
+        }
+    }
+    if (!S.write_xc) {
+        // packed keys order by magnitude, then smallest index: exact first-index ties
+        unsigned long long ka = best_a >= 0.f ? peak_key(best_a, idx_a) : 0ull;
+        unsigned long long kb = best_b >= 0.f ? peak_key(best_b, idx_b) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long xa = __shfl_xor_sync(0xffffffffu, ka, o);
+            const unsigned long long xb = __shfl_xor_sync(0xffffffffu, kb, o);
+            ka = xa > ka ? xa : ka;
+            kb = xb > kb ? xb : kb;
+        }
+        if ((tid & 31) == 0) {
+            if (ka) atomicMax(po.key_a, ka);
+            if (kb && po.key_b) atomicMax(po.key_b, kb);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// One pass over one wave: persistent CTAs, each walking a contiguous range of
+// items with a 2-slot TMA ring (item i+1's bulk copies in flight while item i
+// computes).
+template <int PA, int QA, int PB, int QB, int TYPE>
+__global__ void __launch_bounds__(128, 3) k_corr_pass(const CorrSched S) {
+    using F = Fused<PA, QA, PB, QB>;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smraw);
+    float2* slots = reinterpret_cast<float2*>(smraw + 128);
+    const int n_items = TYPE == 0 ? S.nA : S.nB;
+    const int i0 = int(int64_t(blockIdx.x) * n_items / gridDim.x);
+    const int i1 = int(int64_t(blockIdx.x + 1) * n_items / gridDim.x);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && i0 < i1) {
+        const Ticket k0{TYPE, 0, i0};
+        if (!ticket_noop(S, k0)) issue_ticket<PA, QA, PB, QB>(S, k0, slots, &bar[0]);
+    }
+    uint32_t phases = 0u;   // bit s: parity of slot s's mbarrier
+    for (int item = i0, s = 0; item < i1; ++item, s ^= 1) {
+        if (threadIdx.x == 0 && item + 1 < i1) {
+            const Ticket kn{TYPE, 0, item + 1};
+            if (!ticket_noop(S, kn)) issue_ticket<PA, QA, PB, QB>(S, kn, slots + size_t(s ^ 1) * F::SLOT, &bar[s ^ 1]);
+        }
+        const Ticket k{TYPE, 0, item};
+        if (ticket_noop(S, k)) continue;
+        float2* sl = slots + size_t(s) * F::SLOT;
+        mbar_wait(&bar[s], (phases >> s) & 1u);
+        phases ^= 1u << s;
+        if (TYPE == 0) {
+            item_passA<PA, QA, PB, QB>(S, k, sl);
+        } else {
+            // the M tile is in shared memory and its L2 lines are dead: drop
+            // them without a DRAM write-back (ordered before the ring slot's
+            // reuse by the kernel boundary)
+            const CorrPairOut& po = S.outs[k.idx / S.n_tiles];
+            const char* tile = reinterpret_cast<const char*>(po.M + size_t(k.idx % S.n_tiles) * F::LB * kTileB);
+            if (S.discard)
+                for (int l = threadIdx.x; l < F::LB * kTileB * 8 / 128; l += F::NT) discard_l2(tile + size_t(l) * 128);
+            item_passB<PA, QA, PB, QB>(S, k, sl);
+        }
+        __syncthreads();   // slot s free for the prefetch of item + 2
+    }
+}
+
+}  // namespace tdg

@@ -18,7 +18,7 @@
 
 #include "tagdsp_gpu.h"
 #include "kernels.cuh"
-#include "corr_v2.cuh"
+#include "corr_v3.cuh"
 
 namespace {
 
@@ -205,27 +205,40 @@ double pass_cost(int L) {
     return 1e9;
 }
 
-// Transform length N = N1*N2 >= need minimising N*(cost(N1)+cost(N2)); any
-// N >= W + n - 1 yields the same lags [0, W) (linear correlation).  Between
-// the two orders the pass-A length (N2) is the one with the smaller
-// shared-memory slot, i.e. the smaller length.
+// (N1, N2) splits the fused correlation kernel is instantiated for: the
+// search shape (1024 x 864), the tracking shape (450 x 360) and a power-of-two
+// ladder for everything else (small transforms are padded up; any
+// N >= W + n - 1 gives the same lags [0, W)).
+#define TDG_FUSED(X)                                                              \
+    X(16, 4, 4, 16, 4, 4) X(32, 4, 8, 16, 4, 4) X(32, 4, 8, 32, 4, 8)             \
+    X(64, 8, 8, 32, 4, 8) X(64, 8, 8, 64, 8, 8) X(128, 8, 16, 64, 8, 8)           \
+    X(128, 8, 16, 128, 8, 16) X(256, 16, 16, 128, 8, 16)                          \
+    X(256, 16, 16, 256, 16, 16) X(512, 16, 32, 256, 16, 16)                       \
+    X(512, 16, 32, 512, 16, 32) X(450, 18, 25, 360, 18, 20)                       \
+    X(1024, 32, 32, 512, 16, 32) X(1024, 32, 32, 864, 27, 32)                     \
+    X(1024, 32, 32, 1024, 32, 32)
+
+// Transform length N = N1*N2 >= need minimising N*(cost(N1)+cost(N2)) over
+// the fused splits; any N >= W + n - 1 yields the same lags [0, W) (linear
+// correlation).  N1 (pass B, 32 KB tiles) >= N2 (pass A columns).
 bool choose_corr_len(uint64_t need, int* n1, int* n2) {
     double best = 0.0;
     uint64_t bestN = 0;
     int b1 = 0, b2 = 0;
-    for (const auto& a : kMenu)
-        for (const auto& b : kMenu) {
-            if (a.L < b.L) continue;   // N1 >= N2
-            const uint64_t n = uint64_t(a.L) * uint64_t(b.L);
-            if (n < need) continue;
-            const double c = double(n) * (pass_cost(a.L) + pass_cost(b.L));
-            if (bestN == 0 || c < best * (1.0 - 1e-9) || (c <= best * (1.0 + 1e-9) && n < bestN)) {
-                best = c;
-                bestN = n;
-                b1 = a.L;
-                b2 = b.L;
-            }
+    auto consider = [&](int a, int b) {
+        const uint64_t n = uint64_t(a) * uint64_t(b);
+        if (n < need) return;
+        const double c = double(n) * (pass_cost(a) + pass_cost(b));
+        if (bestN == 0 || c < best * (1.0 - 1e-9) || (c <= best * (1.0 + 1e-9) && n < bestN)) {
+            best = c;
+            bestN = n;
+            b1 = a;
+            b2 = b;
         }
+    };
+#define X(L1, P1, Q1, L2, P2, Q2) consider(L1, L2);
+    TDG_FUSED(X)
+#undef X
     if (!bestN) return false;
     *n1 = b1;
     *n2 = b2;
@@ -304,48 +317,21 @@ int persistent_grid(K* kernel, int threads, size_t smem, int n_items) {
     return std::max(1, std::min(n_items, per_sm * num_sms()));
 }
 
-void launch_corrA(int L, cudaStream_t st, const tdg::CorrGroup<kG>* groups, int n_groups, int N1, const float2* tw) {
-    const int n_items = (N1 / 2 + 1) * n_groups;
-    switch (L) {
-#define X(LL, P, Q)                                                                                 \
-    case LL: {                                                                                      \
-        using C = tdg::PassA2<P, Q, kG>;                                                            \
-        auto* k = tdg::k_corr_passA2<P, Q, kG>;                                                     \
-        const int grid = persistent_grid(k, C::NT, C::SMEM, n_items);                               \
-        k<<<grid, C::NT, C::SMEM, st>>>(groups, n_groups, N1, n_items, tw);                         \
-        LAUNCHED();                                                                                 \
-        return;                                                                                     \
+template <int TYPE>
+void launch_pass(int N1, int N2, cudaStream_t st, const tdg::CorrSched& S) {
+    const int n_items = TYPE == 0 ? S.nA : S.nB;
+#define X(L1, P1, Q1, L2, P2, Q2)                                                       \
+    if (N1 == L1 && N2 == L2) {                                                         \
+        using F = tdg::Fused<P2, Q2, P1, Q1>;                                           \
+        auto* k = tdg::k_corr_pass<P2, Q2, P1, Q1, TYPE>;                               \
+        const int grid = persistent_grid(k, F::NT, F::SMEM, n_items);                   \
+        k<<<grid, F::NT, F::SMEM, st>>>(S);                                             \
+        LAUNCHED();                                                                     \
+        return;                                                                         \
     }
-        TDG_MENU(X)
+    TDG_FUSED(X)
 #undef X
-    }
-    fail(TDG_ERANGE, "corrA: length %d", L);
-}
-
-void launch_corrB(int L, bool write_xc, cudaStream_t st, const tdg::CorrPairOut* pairs, int n_pairs, int N2,
-                  uint32_t W, float inv_n, const float2* tw) {
-    const int n_tiles = (N2 + tdg::kTileB - 1) / tdg::kTileB;
-    const int n_items = n_pairs * n_tiles;
-    switch (L) {
-#define X(LL, P, Q)                                                                                 \
-    case LL: {                                                                                      \
-        using C = tdg::PassB2<P, Q>;                                                                \
-        if (write_xc) {                                                                             \
-            auto* k = tdg::k_corr_passB2<P, Q, true>;                                               \
-            const int grid = persistent_grid(k, C::NT, C::SMEM, n_items);                           \
-            k<<<grid, C::NT, C::SMEM, st>>>(pairs, n_tiles, N2, W, inv_n, n_items, tw);             \
-        } else {                                                                                    \
-            auto* k = tdg::k_corr_passB2<P, Q, false>;                                              \
-            const int grid = persistent_grid(k, C::NT, C::SMEM, n_items);                           \
-            k<<<grid, C::NT, C::SMEM, st>>>(pairs, n_tiles, N2, W, inv_n, n_items, tw);             \
-        }                                                                                           \
-        LAUNCHED();                                                                                 \
-        return;                                                                                     \
-    }
-        TDG_MENU(X)
-#undef X
-    }
-    fail(TDG_ERANGE, "corrB: length %d", L);
+    fail(TDG_ERANGE, "correlation split %d x %d is not instantiated", N1, N2);
 }
 
 // ---------------------------------------------------------------------------
@@ -430,10 +416,28 @@ struct tdg_ctx {
     int clen = 0;
     // scratch
     DevBuf T, M, keys, det_dev, stream_buf;
+    // second stream + events of the two-stream correlation pipeline
+    cudaStream_t stream_b = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    std::vector<cudaEvent_t> ev_a, ev_b;
+    void ensure_pipeline(int ring) {
+        if (!stream_b) CK(cudaStreamCreateWithFlags(&stream_b, cudaStreamNonBlocking));
+        if (!ev_fork) CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+        if (!ev_join) CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+        while (int(ev_a.size()) < ring) {
+            cudaEvent_t a, b;
+            CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+            ev_a.push_back(a);
+            ev_b.push_back(b);
+        }
+    }
     tdg_windows* search_win = nullptr;   // cached window set of tdg_search (reused across calls)
     DescPack pk_fwd, pk_corr, pk_misc;
     std::vector<char> host_stage;
-    int64_t wave_pairs = 8;      // correlation pairs per pass-A/pass-B wave
+    int64_t wave_pairs = 8;      // correlation pairs per wave (one pass-A + one pass-B launch)
+    int64_t ring = 3;            // M wave buffers in flight
+    int64_t discard = 1;         // drop consumed M tiles from L2
     int64_t fwd_wave = 8;        // sequence pairs per forward-FFT wave
     // optional per-launch CUDA-event timing (bench.py roofline)
     bool time_kernels = false;
@@ -486,6 +490,32 @@ struct tdg_ctx {
         CK(cudaMemcpy(buf->p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice));
         const float2* p = buf->as<float2>();
         tw[L] = std::move(buf);
+        return p;
+    }
+
+    // pass-A inter-pass twiddles (csrc/corr_v3.cuh): row k1 = [w_N^{+k1 c}, c < QA]
+    // [w_N^{+k1 QA e}, e < PA], computed in double with exact integer reduction
+    std::map<std::pair<int, int>, std::unique_ptr<DevBuf>> twi;
+    const float2* inter_twiddles(int N1, int N2) {
+        auto key = std::make_pair(N1, N2);
+        auto it = twi.find(key);
+        if (it != twi.end()) return it->second->as<float2>();
+        const PassShape& s = shape_of(N2);
+        const int tws = tdg::inter_tw_stride(s.P, s.Q);
+        const long long N = (long long)N1 * N2;
+        std::vector<float2> h(size_t(N1) * tws, make_float2(0.f, 0.f));
+        const double pi = 3.14159265358979323846;
+        for (int k1 = 0; k1 < N1; ++k1)
+            for (int r = 0; r < s.P + s.Q; ++r) {
+                const long long e = (r < s.Q ? (long long)k1 * r : (long long)k1 * s.Q * (r - s.Q)) % N;
+                const double ang = 2.0 * pi * double(e) / double(N);
+                h[size_t(k1) * tws + r] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
+            }
+        auto buf = std::make_unique<DevBuf>();
+        buf->ensure(h.size() * sizeof(float2));
+        CK(cudaMemcpy(buf->p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice));
+        const float2* p = buf->as<float2>();
+        twi[key] = std::move(buf);
         return p;
     }
 
@@ -649,65 +679,96 @@ struct CorrJob {
     float* xc_b;
 };
 
+// Waves of wave_pairs pairs; pass A of wave w on the context stream, pass B
+// on the second stream, M in a ring of `ring` wave buffers: B(w) waits for
+// A(w), A(w) waits for B(w - ring).  Pass B of wave w thus overlaps pass A of
+// wave w+1 and neither kernel's ramp or tail leaves SMs idle.
 void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const std::vector<CorrJob>& jobs,
                       bool write_xc) {
+    if (jobs.empty()) return;
     const int N1 = cs->N1, N2 = cs->N2;
     const uint64_t N = cs->corr_len(), H = cs->H;
     ensure_dspec(ctx, w, N1, N2);
-    const float2* twA = ctx->twiddles(N2);
-    const float2* twB = ctx->twiddles(N1);
-    const size_t wave = size_t(std::max<int64_t>(kG, ctx->wave_pairs / kG * kG));
-    const uint64_t n_tiles = uint64_t((N2 + tdg::kTileB - 1) / tdg::kTileB);
-    const uint64_t Mstride = n_tiles * uint64_t(N1) * tdg::kTileB;   // tile-major M per pair
-    ctx->M.ensure(wave * Mstride * sizeof(float2));
-    std::vector<tdg::CorrGroup<kG>> groups;
-    std::vector<tdg::CorrPairOut> outs(jobs.size());
-    std::vector<size_t> wave_group0;   // first group index of each wave
-    for (size_t base = 0; base < jobs.size(); base += wave) {
-        const size_t n = std::min(wave, jobs.size() - base);
-        wave_group0.push_back(groups.size());
-        for (size_t i = 0; i < n; ++i) {
-            const CorrJob& jb = jobs[base + i];
-            float2* M = ctx->M.as<float2>() + i * Mstride;
+    constexpr int G = tdg::kGroup;
+    const int wave = int(std::max<int64_t>(G, ctx->wave_pairs / G * G));
+    const int n_waves = int((jobs.size() + size_t(wave) - 1) / size_t(wave));
+    const int ring = int(std::max<int64_t>(1, std::min<int64_t>(ctx->ring, n_waves)));
+    const int n_tiles = (N2 + tdg::kTileB - 1) / tdg::kTileB;
+    const uint64_t Mstride = uint64_t(n_tiles) * uint64_t(N1) * tdg::kTileB;   // tile-major M per pair
+    ctx->M.ensure(size_t(ring) * size_t(wave) * Mstride * sizeof(float2));
+    // groups: consecutive jobs of a wave that share a window spectrum, <= G each
+    std::vector<std::vector<tdg::CorrGroup<G>>> wg(static_cast<size_t>(n_waves));
+    int ngw = 1;
+    for (int wv = 0; wv < n_waves; ++wv) {
+        auto& gs = wg[size_t(wv)];
+        for (int i = 0; i < wave && size_t(wv) * wave + i < jobs.size(); ++i) {
+            const CorrJob& jb = jobs[size_t(wv) * wave + size_t(i)];
             const float2* D = w->dspec.as<float2>() + jb.slot * H;
-            if (groups.size() == wave_group0.back() || groups.back().npairs == kG || groups.back().D != D) {
-                tdg::CorrGroup<kG> g{};
+            if (gs.empty() || gs.back().npairs == G || gs.back().D != D) {
+                tdg::CorrGroup<G> g{};
                 g.D = D;
-                g.npairs = 0;
-                groups.push_back(g);
+                gs.push_back(g);
             }
-            auto& g = groups.back();
+            auto& g = gs.back();
             g.Ca[g.npairs] = cs->spec.as<float2>() + jb.pair * N;
             g.Cb[g.npairs] = nullptr;
-            g.M[g.npairs] = M;
+            g.M[g.npairs] = ctx->M.as<float2>() + (size_t(wv % ring) * wave + size_t(i)) * Mstride;
             ++g.npairs;
-            auto& o = outs[base + i];
-            o.M = M;
+        }
+        ngw = std::max(ngw, int(gs.size()));
+    }
+    std::vector<tdg::CorrGroup<G>> groups(size_t(n_waves) * ngw);   // npairs 0 = no-op item
+    std::vector<tdg::CorrPairOut> outs(size_t(n_waves) * wave);     // M null = no-op item
+    for (int wv = 0; wv < n_waves; ++wv) {
+        for (size_t g = 0; g < wg[size_t(wv)].size(); ++g) groups[size_t(wv) * ngw + g] = wg[size_t(wv)][g];
+        for (int i = 0; i < wave && size_t(wv) * wave + i < jobs.size(); ++i) {
+            const CorrJob& jb = jobs[size_t(wv) * wave + size_t(i)];
+            auto& o = outs[size_t(wv) * wave + size_t(i)];
+            o.M = ctx->M.as<float2>() + (size_t(wv % ring) * wave + size_t(i)) * Mstride;
             o.key_a = jb.key_a;
             o.key_b = jb.key_b;
             o.xc_a = jb.xc_a;
             o.xc_b = jb.xc_b;
         }
     }
-    wave_group0.push_back(groups.size());
     ctx->pk_corr.begin();
     const size_t og = ctx->pk_corr.add(groups);
     const size_t oo = ctx->pk_corr.add(outs);
     ctx->pk_corr.commit(ctx->stream);
-    auto* gd = ctx->pk_corr.at<tdg::CorrGroup<kG>>(og);
+    tdg::CorrSched S{};
+    S.twA = ctx->twiddles(N2);
+    S.twB = ctx->twiddles(N1);
+    S.twI = ctx->inter_twiddles(N1, N2);
+    S.ngw = ngw;
+    S.wave_pairs = wave;
+    S.n_tiles = n_tiles;
+    S.nA = (N1 / 2 + 1) * ngw;
+    S.nB = wave * n_tiles;
+    S.N1 = N1;
+    S.N2 = N2;
+    S.write_xc = write_xc ? 1 : 0;
+    S.discard = ctx->discard ? 1 : 0;
+    S.W = uint32_t(w->W);
+    S.inv_n = 1.0f / float(N);
+    auto* gd = ctx->pk_corr.at<tdg::CorrGroup<G>>(og);
     auto* od = ctx->pk_corr.at<tdg::CorrPairOut>(oo);
-    for (size_t wv = 0, base = 0; base < jobs.size(); ++wv, base += wave) {
-        const size_t n = std::min(wave, jobs.size() - base);
-        const size_t g0 = wave_group0[wv], g1 = wave_group0[wv + 1];
-        {
-            KScope ks(ctx, "corr_passA");
-            launch_corrA(N2, ctx->stream, gd + g0, int(g1 - g0), N1, twA);
-        }
-        {
-            KScope ks(ctx, "corr_passB");
-            launch_corrB(N1, write_xc, ctx->stream, od + base, int(n), N2, uint32_t(w->W), 1.0f / float(N), twB);
-        }
+    ctx->ensure_pipeline(ring);
+    KScope ks(ctx, "corr");   // spans both streams: the B stream joins back below
+    CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->stream_b, ctx->ev_fork, 0));
+    for (int wv = 0; wv < n_waves; ++wv) {
+        const int r = wv % ring;
+        S.groups = gd + size_t(wv) * ngw;
+        S.outs = od + size_t(wv) * wave;
+        if (wv >= ring) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_b[size_t(r)], 0));
+        launch_pass<0>(N1, N2, ctx->stream, S);
+        CK(cudaEventRecord(ctx->ev_a[size_t(r)], ctx->stream));
+        CK(cudaStreamWaitEvent(ctx->stream_b, ctx->ev_a[size_t(r)], 0));
+        launch_pass<1>(N1, N2, ctx->stream_b, S);
+        CK(cudaEventRecord(ctx->ev_b[size_t(r)], ctx->stream_b));
     }
+    CK(cudaEventRecord(ctx->ev_join, ctx->stream_b));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
 }
 
 }  // namespace
@@ -740,6 +801,11 @@ void tdg_ctx_destroy(tdg_ctx* ctx) {
     }
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->search_win) tdg_windows_destroy(ctx->search_win);
+    for (auto e : ctx->ev_a) cudaEventDestroy(e);
+    for (auto e : ctx->ev_b) cudaEventDestroy(e);
+    if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->stream_b) cudaStreamDestroy(ctx->stream_b);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -787,6 +853,11 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
             ctx->time_kernels = value != 0;
         } else if (k == "wave_pairs")
             ctx->wave_pairs = value > 0 ? value : 8;
+        else if (k == "discard")
+            ctx->discard = value;
+        else if (k == "ring")
+            ctx->ring = value > 0 ? value : 3;
+
         else if (k == "fwd_wave")
             ctx->fwd_wave = value > 0 ? value : 8;
         else
@@ -1086,10 +1157,14 @@ void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float thre
     CK(cudaMemsetAsync(ctx->keys.p, 0, ns * nc * sizeof(unsigned long long), ctx->stream));
     std::vector<CorrJob> jobs;
     unsigned long long* keys = ctx->keys.as<unsigned long long>();
-    for (uint64_t s = 0; s < ns; ++s)
-        for (uint64_t p = 0; 2 * p < nc; ++p)
-            jobs.push_back({s, p, keys + s * nc + 2 * p, 2 * p + 1 < nc ? keys + s * nc + 2 * p + 1 : nullptr,
-                            nullptr, nullptr});
+    // code-pair-major: a group of kGroup stored pairs (whose spectra stay
+    // L2-resident) sweeps every window slot before the next group starts
+    const uint64_t npairs = (nc + 1) / 2, G = tdg::kGroup;
+    for (uint64_t p0 = 0; p0 < npairs; p0 += G)
+        for (uint64_t s = 0; s < ns; ++s)
+            for (uint64_t p = p0; p < std::min(npairs, p0 + G); ++p)
+                jobs.push_back({s, p, keys + s * nc + 2 * p, 2 * p + 1 < nc ? keys + s * nc + 2 * p + 1 : nullptr,
+                                nullptr, nullptr});
     run_correlations(ctx, w, cs, jobs, false);
     ctx->det_dev.ensure(ns * nc * sizeof(tdg_detection));
     std::vector<tdg::StatsDesc> sd(ns * nc);

@@ -20,13 +20,14 @@ bench)
 benchfast)
   timeout 600 python bench.py --no-cpu-baseline > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err ;;
 launches)
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -s 1000 -c 1200 --csv \
-      --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/launches_bench.log 2>&1 ;;
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --cache-control none --clock-control none --profile-from-start off --csv \
+      --log-file $OUT/launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --profile-step > $OUT/launches_bench.log 2>&1 ;;
 ncu)
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_corr_passA2 -s 40 -c 1 \
-      -o $OUT/passA python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncuA.log 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_corr_passB2 -s 40 -c 1 \
-      -o $OUT/passB python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncuB.log 2>&1 ;;
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_corr_pass --profile-from-start off -c 2 \
+      -o $OUT/corr python bench.py --steps 1 --warmup 3 --no-cpu-baseline --profile-step > $OUT/ncuA.log 2>&1
+  true ;;
+sweep)
+  timeout 600 python tools/sweep.py $SWEEP > $OUT/sweep.log 2>&1 ;;
 esac
 done
 ls -la $OUT

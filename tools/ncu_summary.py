@@ -7,6 +7,7 @@
 import collections
 import csv
 import io
+import json
 import subprocess
 import sys
 
@@ -58,29 +59,40 @@ def full(rep):
     print()
 
 
-def launches(path):
-    agg = collections.defaultdict(lambda: [0, 0.0])
+def launches(path, traffic_out=None):
+    """Per-kernel time share; with dram__bytes_{read,write}.sum in the list
+    (ncu --cache-control none), also the warm-L2 DRAM traffic per kernel."""
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
     with open(path) as f:
         txt = [l for l in f if l.startswith('"')]
+    scale = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+    bscale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
     for r in csv.DictReader(io.StringIO("".join(txt))):
-        if r.get("Metric Name") != "gpu__time_duration.sum":
-            continue
         k = r["Kernel Name"].split("(")[0].replace("void ", "")
         v = float(r["Metric Value"].replace(",", ""))
-        v *= {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3, "nsecond": 1e-3}.get(r["Metric Unit"], 1.0)
-        agg[k][0] += 1
-        agg[k][1] += v
+        if r.get("Metric Name") == "gpu__time_duration.sum":
+            agg[k][0] += 1
+            agg[k][1] += v * scale.get(r["Metric Unit"], 1.0)
+        elif r.get("Metric Name", "").startswith("dram__bytes_"):
+            agg[k][2] += v * bscale.get(r["Metric Unit"], 1.0)
     tot = sum(a[1] for a in agg.values())
-    print("| kernel | launches | total us | share | avg us |\n|---|---|---|---|---|")
-    for k, (n, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
-        print("| `%s` | %d | %.1f | %.1f%% | %.2f |" % (k, n, t, 100 * t / tot, t / n))
-    print("\nTotal %.1f us over %d launches (serialised, cold-cache: compare shares)." %
+    print("| kernel | launches | total us | share | avg us | DRAM bytes (warm) |\n|---|---|---|---|---|---|")
+    for k, (n, t, b) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print("| `%s` | %d | %.1f | %.1f%% | %.2f | %s |" % (k, n, t, 100 * t / tot, t / n,
+                                                          "%.3g" % b if b else "-"))
+    print("\nTotal %.1f us over %d launches (serialised by ncu: compare shares)." %
           (tot, sum(a[0] for a in agg.values())))
+    if traffic_out:
+        corr = sum(b for k, (n, t, b) in agg.items() if k.startswith("k_corr"))
+        with open(traffic_out, "w") as f:
+            json.dump({"corr_dram_bytes_per_step": corr, "source": path,
+                       "note": "sum of dram__bytes_read.sum + dram__bytes_write.sum over the correlation "
+                               "launches of one bench step, ncu --cache-control none (warm L2)"}, f, indent=1)
 
 
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
-        launches(sys.argv[2])
+        launches(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
     else:
         for rep in sys.argv[2:]:
             full(rep)
