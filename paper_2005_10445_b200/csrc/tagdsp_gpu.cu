@@ -317,6 +317,8 @@ int persistent_grid(K* kernel, int threads, size_t smem, int n_items) {
     return std::max(1, std::min(n_items, per_sm * num_sms()));
 }
 
+int g_cta_cap[2] = {0, 0};   // tuning: max CTAs per SM of pass A / pass B (0 = occupancy)
+
 template <int TYPE>
 void launch_pass(int N1, int N2, cudaStream_t st, const tdg::CorrSched& S) {
     const int n_items = TYPE == 0 ? S.nA : S.nB;
@@ -324,7 +326,8 @@ void launch_pass(int N1, int N2, cudaStream_t st, const tdg::CorrSched& S) {
     if (N1 == L1 && N2 == L2) {                                                         \
         using F = tdg::Fused<P2, Q2, P1, Q1>;                                           \
         auto* k = tdg::k_corr_pass<P2, Q2, P1, Q1, TYPE>;                               \
-        const int grid = persistent_grid(k, F::NT, F::SMEM, n_items);                   \
+        int grid = persistent_grid(k, F::NT, F::SMEM, n_items);                         \
+        if (g_cta_cap[TYPE] > 0) grid = std::min(grid, g_cta_cap[TYPE] * num_sms());   \
         k<<<grid, F::NT, F::SMEM, st>>>(S);                                             \
         LAUNCHED();                                                                     \
         return;                                                                         \
@@ -438,6 +441,7 @@ struct tdg_ctx {
     int64_t wave_pairs = 8;      // correlation pairs per wave (one pass-A + one pass-B launch)
     int64_t ring = 3;            // M wave buffers in flight
     int64_t discard = 1;         // drop consumed M tiles from L2
+    int64_t one_stream = 0;      // tuning: run pass B on the context stream too (no overlap)
     int64_t fwd_wave = 8;        // sequence pairs per forward-FFT wave
     // optional per-launch CUDA-event timing (bench.py roofline)
     bool time_kernels = false;
@@ -763,9 +767,10 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
         if (wv >= ring) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_b[size_t(r)], 0));
         launch_pass<0>(N1, N2, ctx->stream, S);
         CK(cudaEventRecord(ctx->ev_a[size_t(r)], ctx->stream));
-        CK(cudaStreamWaitEvent(ctx->stream_b, ctx->ev_a[size_t(r)], 0));
-        launch_pass<1>(N1, N2, ctx->stream_b, S);
-        CK(cudaEventRecord(ctx->ev_b[size_t(r)], ctx->stream_b));
+        cudaStream_t sb = ctx->one_stream ? ctx->stream : ctx->stream_b;
+        CK(cudaStreamWaitEvent(sb, ctx->ev_a[size_t(r)], 0));
+        launch_pass<1>(N1, N2, sb, S);
+        CK(cudaEventRecord(ctx->ev_b[size_t(r)], sb));
     }
     CK(cudaEventRecord(ctx->ev_join, ctx->stream_b));
     CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
@@ -853,6 +858,12 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
             ctx->time_kernels = value != 0;
         } else if (k == "wave_pairs")
             ctx->wave_pairs = value > 0 ? value : 8;
+        else if (k == "cta_cap_a")
+            g_cta_cap[0] = int(value);
+        else if (k == "cta_cap_b")
+            g_cta_cap[1] = int(value);
+        else if (k == "one_stream")
+            ctx->one_stream = value;
         else if (k == "discard")
             ctx->discard = value;
         else if (k == "ring")

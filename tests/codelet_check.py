@@ -1,10 +1,30 @@
-"""Execute the generated CUDA codelets on the CPU by translating their
-straight-line bodies to Python, and compare with a float64 DFT."""
+"""Execute the generated CUDA codelets (csrc/codelets.cuh, packed f32x2
+form written by tools/gen_codelets2.py) on the CPU by translating their
+straight-line bodies to Python, and compare with a float64 DFT.
+
+A packed value (64-bit register pair, lo = re, hi = im) is modelled as a
+Python complex whose real/imag parts are the two lanes; the PTX f32x2 ops
+act lane-wise."""
 import re
 
 import numpy as np
 
 _HDR = re.compile(r"template <> __device__ __forceinline__ void dft<(\d+), (-?\d+)>\(float2 \(&x\)\[\d+\]\) \{\n(.*?)\n\}\n", re.S)
+
+
+def _lanes(f):
+    return lambda *a: complex(f(*[z.real for z in a]), f(*[z.imag for z in a]))
+
+
+ENV = {
+    "pk": lambda lo, hi: complex(lo, hi),
+    "up": lambda v: v,
+    "swp": lambda v: complex(v.imag, v.real),
+    "add2": _lanes(lambda a, b: a + b),
+    "sub2": _lanes(lambda a, b: a - b),
+    "mul2": _lanes(lambda a, b: a * b),
+    "fma2": _lanes(lambda a, b, c: a * b + c),
+}
 
 
 def parse_codelets(path):
@@ -14,14 +34,12 @@ def parse_codelets(path):
         n, sign, body = int(m.group(1)), int(m.group(2)), m.group(3)
         py = []
         for line in body.splitlines():
-            line = line.strip()
-            if line.startswith("const float "):
-                line = line[len("const float "):].rstrip(";")
-            elif line.startswith("x[") and "make_float2" in line:
+            line = line.strip().rstrip(";")
+            if line.startswith("const c2 "):
+                line = line[len("const c2 "):]
+            elif line.startswith("x[") and "= up(" in line:
                 k = line[2:line.index("]")]
-                args = line[line.index("make_float2(") + len("make_float2("):line.rindex(")")]
-                a, b = [s.strip() for s in args.split(",")]
-                line = f"out[{k}] = complex({a}, {b})"
+                line = f"out[{k}] = {line[line.index('=') + 1:].strip()}"
             line = re.sub(r"x\[(\d+)\]\.x", r"x[\1].real", line)
             line = re.sub(r"x\[(\d+)\]\.y", r"x[\1].imag", line)
             line = re.sub(r"(\d\.\d*(?:e[-+]?\d+)?)f\b", r"\1", line)
@@ -31,7 +49,7 @@ def parse_codelets(path):
 
 
 def run_codelet(code, x):
-    env = {"x": list(x), "out": [0j] * len(x), "complex": complex}
+    env = dict(ENV, x=list(x), out=[0j] * len(x))
     exec(code, env)
     return np.array(env["out"])
 

@@ -23,17 +23,22 @@ def near_tie_margin(xc_ref, j_ref, j_gpu):
     return (a - b) / a if a else 0.0
 
 
-def delta_tolerance(xc_ref, j, delta, eps):
-    """Bound on |subsample_offset| differences caused by relative perturbations
-    eps of the xc values: delta = 0.5(a-c)/(a-2b+c) (detector.cpp:136-145) has
-    |d delta| <= eps*b*(1+2|delta|)/|a-2b+c|, plus a 1e-4 floor."""
+def delta_tolerance(xc_ref, j, delta, eps, xc_scale=0.0):
+    """Bound on |subsample_offset| differences caused by perturbations of the
+    xc values: delta = 0.5(a-c)/(a-2b+c) (detector.cpp:136-145) has
+    |d delta| <= e*(1+2|delta|)/|a-2b+c| for an absolute perturbation e of
+    a, b, c, plus a 1e-4 floor.  e = eps * max(b, xc_scale): a rounding-level
+    difference of the replica or window (two FFT implementations) perturbs
+    each lag by ~eps relative to the Cauchy-Schwarz scale sqrt(q*E) =
+    |w_c/score| of the dot product, which for a weak (absent-code) peak is
+    far above b itself."""
     if xc_ref is None or j == 0 or j + 1 >= len(xc_ref):
         return 1e-4
     a, b, c = (abs(float(xc_ref[j - 1])), abs(float(xc_ref[j])), abs(float(xc_ref[j + 1])))
     den = abs(a - 2.0 * b + c)
     if den == 0.0:
         return 1e-4
-    return 1e-4 + eps * b * (1.0 + 2.0 * abs(delta)) / den
+    return 1e-4 + eps * max(b, xc_scale) * (1.0 + 2.0 * abs(delta)) / den
 
 
 def compare_detections(got, want, sample_rate, tie_ok=None, rel=REL, xc_ref=None, eps=2e-6):
@@ -60,7 +65,8 @@ def compare_detections(got, want, sample_rate, tie_ok=None, rel=REL, xc_ref=None
             if abs(gv - wv) > rel * abs(wv) + 1e-7:
                 bad.append((key, f, gv, wv))
         xr = None if xc_ref is None else xc_ref[int(w["code_index"])]
-        dtol = delta_tolerance(xr, int(w["peak_index"]), float(w["subsample_offset"]), eps)
+        sc = abs(float(w["w_c"]) / float(w["score"])) if float(w["score"]) else 0.0
+        dtol = delta_tolerance(xr, int(w["peak_index"]), float(w["subsample_offset"]), eps, sc)
         if abs(float(g["subsample_offset"]) - float(w["subsample_offset"])) > dtol:
             bad.append((key, "subsample_offset", float(g["subsample_offset"]), float(w["subsample_offset"]), dtol))
         if abs(float(g["toa_seconds"]) - float(w["toa_seconds"])) * sample_rate > dtol + 1e-6:
