@@ -132,7 +132,22 @@ int tdg_search(tdg_ctx* ctx, const tdg_demod_config* cfg, const double* lo_bins,
                uint64_t advance, const tdg_codeset* cs, float threshold, tdg_detection* out,
                uint64_t out_cap, uint64_t* n_out);
 
-/* Tuning / profiling knobs (0 = default): "wave_pairs", "fwd_wave",
+/* Tracking mode: a batch of short windows, one code each (what
+ * proj/src/recording.cpp:360-378 does per Tracking task: demodulate_window
+ * at cfg->lo_freq, prepare_code(track_shape) -> detect with that one code).
+ * iq covers stream samples [stream_start, stream_start + n_complex); every
+ * task window must lie inside it; the code set must be prepared for the
+ * tracking window length.  out[i] is task i's Detection (accepted or not).
+ * _device: iq is a device pointer (e.g. a device-resident ring buffer). */
+int tdg_track(tdg_ctx* ctx, const tdg_demod_config* cfg, const int16_t* iq, uint64_t n_complex,
+              int64_t stream_start, const tdg_track_task* tasks, uint64_t n_tasks, const tdg_codeset* cs,
+              float threshold, tdg_detection* out);
+int tdg_track_device(tdg_ctx* ctx, const tdg_demod_config* cfg, const int16_t* iq_dev, uint64_t n_complex,
+                     int64_t stream_start, const tdg_track_task* tasks, uint64_t n_tasks,
+                     const tdg_codeset* cs, float threshold, tdg_detection* out);
+
+/* Tuning / profiling knobs (0 = default): "wave_pairs", "ring", "discard",
+ * "fwd_wave", "one_stream", "cta_cap_a", "cta_cap_b",
  * "time_kernels" (1 = record a CUDA event pair on the context stream around
  * every launch; read back with tdg_kernel_time). */
 int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value);

@@ -52,6 +52,14 @@ typedef struct tdg_detection {
     uint8_t reserved[6];
 } tdg_detection;
 
+/* One tracking task (tagdsp::Task of kind Tracking, include/tagdsp/scheduler.hpp
+ * and proj/src/scheduler.cpp:89-113): the window [start, start + window_len)
+ * of the stream, searched for exactly one code. */
+typedef struct tdg_track_task {
+    int64_t start;         /* absolute stream index of the window's first sample */
+    uint64_t code_index;   /* code in the code set (prepared for the tracking window length) */
+} tdg_track_task;
+
 /* Status codes of every C-ABI entry point (0 = ok).  The C++ wrapper maps
  * TDG_EINVAL to std::invalid_argument (the reference's precondition
  * exceptions) and everything else to std::runtime_error. */

@@ -64,3 +64,7 @@ def packet_samples(cfg):
 
 def composed_filter_len(cfg):
     return int(cfg.bandpass_taps) + samples_per_bit(cfg) - 1
+
+
+# tdg_track_task (include/tagdsp_gpu_types.h)
+TRACK_TASK_DTYPE = np.dtype([("start", np.int64), ("code_index", np.uint64)])

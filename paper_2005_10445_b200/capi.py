@@ -11,6 +11,7 @@ call raises.  Names and argument meaning follow the reference
   batch_xcorr(ctx, windows, slot, codes, idx) detector.hpp:75-77
   detect(ctx, windows, codes, threshold, fs)  detector.hpp:103-106
   search(ctx, cfg, bins, iq, ...)             recording.cpp:258-289 (detect_recording)
+  track(ctx, cfg, iq, tasks, codes)           recording.cpp:360-378 (tracking tasks, batched)
 
 Errors: TDG_EINVAL -> InvalidArgument (a ValueError, the reference's
 std::invalid_argument), anything else -> GpuError (RuntimeError).
@@ -20,7 +21,7 @@ import os
 
 import numpy as np
 
-from ._abi import DETECTION_DTYPE, DemodConfig, demod_config, desk_config  # noqa: F401
+from ._abi import DETECTION_DTYPE, TRACK_TASK_DTYPE, DemodConfig, demod_config, desk_config  # noqa: F401
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtagdsp_gpu.so")
@@ -69,6 +70,10 @@ _PROTOS = {
     "tdg_batch_xcorr": (ctypes.c_int, [_P, _P, _U64, _P, _P, _U64, _P]),
     "tdg_search": (ctypes.c_int, [_P, ctypes.POINTER(DemodConfig), _P, _U64, _P, _U64, _I64, _U64, _U64, _P,
                                   ctypes.c_float, _P, _U64, ctypes.POINTER(_U64)]),
+    "tdg_track": (ctypes.c_int, [_P, ctypes.POINTER(DemodConfig), _P, _U64, _I64, _P, _U64, _P, ctypes.c_float,
+                                 _P]),
+    "tdg_track_device": (ctypes.c_int, [_P, ctypes.POINTER(DemodConfig), _P, _U64, _I64, _P, _U64, _P,
+                                        ctypes.c_float, _P]),
     "tdg_set_option": (ctypes.c_int, [_P, ctypes.c_char_p, _I64]),
     "tdg_kernel_time": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.POINTER(_U64), ctypes.POINTER(ctypes.c_double)]),
     "tdg_kernel_time_reset": (ctypes.c_int, [_P]),
@@ -330,3 +335,18 @@ def search(ctx, cfg, lo_bins, iq, codes, window_len, advance, threshold=0.25, st
                             int(window_len), int(advance), codes._h, float(threshold), _ptr(out), out.size,
                             ctypes.byref(n_out)))
     return out[:n_out.value]
+
+
+def track(ctx, cfg, iq, starts, code_idx, codes, threshold=0.25, stream_start=0):
+    """Tracking tasks (proj/src/recording.cpp:360-378, one scheduler Task of
+    kind Tracking each): window [starts[i], starts[i] + codes.window_len)
+    demodulated at cfg.lo_freq and detected against code code_idx[i].
+    Returns DETECTION_DTYPE records, one per task."""
+    iq = np.ascontiguousarray(iq, dtype=np.int16)
+    tasks = np.zeros(len(starts), dtype=TRACK_TASK_DTYPE)
+    tasks["start"] = starts
+    tasks["code_index"] = code_idx
+    out = np.zeros(tasks.size, dtype=DETECTION_DTYPE)
+    _check(lib().tdg_track(ctx.handle, ctypes.byref(cfg), _ptr(iq), iq.size // 2, int(stream_start), _ptr(tasks),
+                           tasks.size, codes._h, float(threshold), _ptr(out)))
+    return out

@@ -436,6 +436,7 @@ struct tdg_ctx {
         }
     }
     tdg_windows* search_win = nullptr;   // cached window set of tdg_search (reused across calls)
+    tdg_windows* track_win = nullptr;    // cached window set of tdg_track (capacity grows)
     DescPack pk_fwd, pk_corr, pk_misc;
     std::vector<char> host_stage;
     int64_t wave_pairs = 8;      // correlation pairs per wave (one pass-A + one pass-B launch)
@@ -615,7 +616,9 @@ struct tdg_windows {
     std::vector<int64_t> start;   // window_start per slot
     DevBuf dspec;
     uint64_t dspec_N = 0;         // transform length dspec was computed for (0 = stale)
+    uint64_t active = 0;          // slots in use (tracking batches reuse a larger set); 0 = all
     uint64_t slots() const { return n_windows * n_bins; }
+    uint64_t used() const { return active ? active : slots(); }
 };
 
 namespace {
@@ -663,8 +666,8 @@ void ensure_dspec(tdg_ctx* ctx, tdg_windows* w, int N1, int N2) {
     const uint64_t H = uint64_t(N1 / 2 + 1) * uint64_t(N2);
     w->dspec.ensure(w->slots() * H * sizeof(float2));
     std::vector<FwdJob> jobs;
-    for (uint64_t s = 0; s < w->slots(); s += 2) {
-        const bool two = s + 1 < w->slots();
+    for (uint64_t s = 0; s < w->used(); s += 2) {
+        const bool two = s + 1 < w->used();
         jobs.push_back({w->d.as<float>() + s * w->W, two ? w->d.as<float>() + (s + 1) * w->W : nullptr, w->W,
                         two ? w->W : 0, w->dspec.as<float2>() + s * H, two ? w->dspec.as<float2>() + (s + 1) * H : nullptr});
     }
@@ -806,6 +809,7 @@ void tdg_ctx_destroy(tdg_ctx* ctx) {
     }
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     if (ctx->search_win) tdg_windows_destroy(ctx->search_win);
+    if (ctx->track_win) tdg_windows_destroy(ctx->track_win);
     for (auto e : ctx->ev_a) cudaEventDestroy(e);
     for (auto e : ctx->ev_b) cudaEventDestroy(e);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
@@ -1261,6 +1265,113 @@ int tdg_search(tdg_ctx* ctx, const tdg_demod_config* cfg, const double* lo_bins,
         demodulate_impl(ctx, w, cfg, lo_bins, n_bins, ctx->stream_buf.as<int16_t>(), n_complex, stream_start, advance,
                         n_windows);
         detect_impl(ctx, w, cs, threshold, cfg->mod.sample_rate, out);
+    });
+}
+
+
+// ---------------------------------------------------------------------------
+// Tracking (proj/src/recording.cpp:360-378, one Task of
+// proj/src/scheduler.cpp:89-113 each): every task is a short window
+// [start, start + W) demodulated at cfg->lo_freq and detected against ONE
+// code.  A batch of tasks runs as one pipeline: one demod launch for all
+// windows, the forward transforms, one correlation job per task and one
+// statistics launch -- the latency-bound small batches of BASELINE configs[3].
+namespace {
+void track_impl(tdg_ctx* ctx, const tdg_demod_config* cfg, const int16_t* iq_dev, uint64_t n_complex,
+                int64_t stream_start, const tdg_track_task* tasks, uint64_t n_tasks, const tdg_codeset* cs,
+                float threshold, tdg_detection* out) {
+    const uint64_t W = cs->window_len;
+    for (uint64_t i = 0; i < n_tasks; ++i) {
+        if (tasks[i].code_index >= cs->n_codes) fail(TDG_EINVAL, "track: task %llu code index out of range",
+                                                     (unsigned long long)i);
+        if (tasks[i].start < stream_start || uint64_t(tasks[i].start - stream_start) + W > n_complex)
+            fail(TDG_EINVAL, "track: task %llu window outside the sample block", (unsigned long long)i);
+        if (W + cs->nlen[tasks[i].code_index] > cs->corr_len() + 1)
+            fail(TDG_EINVAL, "batch_xcorr: window does not fit transform size");
+    }
+    tdg_windows* w = ctx->track_win;
+    if (!w || w->W != W || w->n_windows < n_tasks) {
+        if (w) tdg_windows_destroy(w);
+        ctx->track_win = nullptr;
+        uint64_t cap = 16;
+        while (cap < n_tasks) cap *= 2;
+        int rc = tdg_windows_create(ctx, W, cap, 1, &w);
+        if (rc) fail(rc, "%s", g_err.c_str());
+        ctx->track_win = w;
+    }
+    w->active = n_tasks;
+    const std::vector<double> bins{cfg->lo_freq};
+    const float2* H = ctx->filter_spectra(*cfg, bins);
+    std::vector<tdg::DemodWindowDesc> wins(n_tasks);
+    for (uint64_t i = 0; i < n_tasks; ++i) {
+        wins[i] = {uint64_t(tasks[i].start - stream_start), w->d.as<float>() + i * W, w->u.as<float>() + i * W};
+        w->start[i] = tasks[i].start;
+    }
+    demod_launch(ctx, iq_dev, true, n_complex, wins, W, 1, W, H, cfg->eps);
+    w->dspec_N = 0;
+    // keys[i]: argmax of task i; keys[n_tasks]: sink for the stored pair's
+    // other code (its correlation comes for free in the packed IFFT)
+    ctx->keys.ensure((n_tasks + 1) * sizeof(unsigned long long));
+    CK(cudaMemsetAsync(ctx->keys.p, 0, (n_tasks + 1) * sizeof(unsigned long long), ctx->stream));
+    unsigned long long* keys = ctx->keys.as<unsigned long long>();
+    std::vector<CorrJob> jobs(n_tasks);
+    for (uint64_t i = 0; i < n_tasks; ++i) {
+        const uint64_t c = tasks[i].code_index;
+        const bool odd = c % 2 != 0;
+        jobs[i] = {i, c / 2, odd ? keys + n_tasks : keys + i, odd ? keys + i : nullptr, nullptr, nullptr};
+    }
+    run_correlations(ctx, w, cs, jobs, false);
+    ctx->det_dev.ensure(n_tasks * sizeof(tdg_detection));
+    std::vector<tdg::StatsDesc> sd(n_tasks);
+    for (uint64_t i = 0; i < n_tasks; ++i) {
+        const uint64_t c = tasks[i].code_index;
+        auto& x = sd[i];
+        x.d = w->d.as<float>() + i * W;
+        x.u = w->u.as<float>() + i * W;
+        x.dc = cs->rep.as<float>() + c * cs->rep_cap;
+        x.key = keys + i;
+        x.out = ctx->det_dev.as<tdg_detection>() + i;
+        x.nonzero_len = uint32_t(cs->nlen[c]);
+        x.energy = cs->energy[c];
+        x.window_start = tasks[i].start;
+        x.code_index = int32_t(c);
+        x.bin = 0;
+    }
+    auto* sdd = ctx->upload(ctx->pk_misc, sd);
+    {
+        KScope ks(ctx, "stats");
+        tdg::k_stats<<<unsigned(n_tasks), 256, 0, ctx->stream>>>(sdd, uint32_t(W), cfg->mod.sample_rate, threshold);
+        LAUNCHED();
+    }
+    if (out) {
+        CK(cudaMemcpyAsync(out, ctx->det_dev.p, n_tasks * sizeof(tdg_detection), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+}
+}  // namespace
+
+int tdg_track_device(tdg_ctx* ctx, const tdg_demod_config* cfg, const int16_t* iq_dev, uint64_t n_complex,
+                     int64_t stream_start, const tdg_track_task* tasks, uint64_t n_tasks, const tdg_codeset* cs,
+                     float threshold, tdg_detection* out) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (n_tasks == 0) return;
+        track_impl(ctx, cfg, iq_dev, n_complex, stream_start, tasks, n_tasks, cs, threshold, out);
+    });
+}
+
+int tdg_track(tdg_ctx* ctx, const tdg_demod_config* cfg, const int16_t* iq, uint64_t n_complex, int64_t stream_start,
+              const tdg_track_task* tasks, uint64_t n_tasks, const tdg_codeset* cs, float threshold,
+              tdg_detection* out) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (n_tasks == 0) return;
+        ctx->stream_buf.ensure(n_complex * 2 * sizeof(int16_t));
+        CK(cudaMemcpyAsync(ctx->stream_buf.p, iq, n_complex * 2 * sizeof(int16_t), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        track_impl(ctx, cfg, ctx->stream_buf.as<int16_t>(), n_complex, stream_start, tasks, n_tasks, cs, threshold,
+                   out);
     });
 }
 

@@ -277,3 +277,60 @@ def test_invalid_arguments_raise(gpu_ctx):
         capi.detect(gpu_ctx, w, cs)                               # mixed window shapes
     with pytest.raises(capi.InvalidArgument):
         capi.demodulate_window(gpu_ctx, np.zeros(3, np.int16), 0, cfg)   # odd raw count
+
+
+def test_tracking_batch_parity(gpu_ctx, ref):
+    """Tracking mode (BASELINE configs[3]; proj/src/recording.cpp:360-378 per
+    scheduler Task): a batch of 12 ms windows [toa - 2 ms, toa + 10 ms) at the
+    default 8 Ms/s, one code each, through tdg_track against the reference's
+    demodulate_window + prepare_code(track_shape) + detect per task.  Covers
+    injected codes (accepted), absent codes, odd/even code slots of a stored
+    pair and overlapping windows."""
+    from paper_2005_10445_b200 import capi
+    from paper_2005_10445_b200._abi import demod_config
+    cfg = demod_config()
+    fs = cfg.mod.sample_rate
+    W = 96000                     # (track_pre_s + track_post_s) * fs, scheduler.hpp:68-69
+    pre = 16000
+    seeds = [2000 + i for i in range(5)]
+    bits = np.stack([ref.gen_code(s, cfg) for s in seeds])
+    inj = [(0, 0.0103, 1.0, 0.0), (3, 0.0412, 0.8, 0.0), (1, 0.0707, 1.0, 0.0)]
+    iq = ref.generate_recording(cfg, seeds, 0.1, 10.0, 77, inj)
+    n = iq.size // 2
+    toas = [int(round(t * fs)) for _, t, _, _ in inj]
+    starts = [toas[0] - pre, toas[1] - pre, toas[2] - pre, toas[0] - pre, toas[1] - pre + 5000, 30000]
+    codes = [0, 3, 1, 2, 3, 4]    # tasks 3, 5: absent codes; task 4: shifted window
+    assert all(0 <= s0 and s0 + W <= n for s0 in starts)
+    cs = capi.CodeSet.prepare(gpu_ctx, cfg, W, bits)
+    dets = capi.track(gpu_ctx, cfg, iq, starts, codes, cs, 0.25)
+    s = ref.Session()
+    idx = [s.prepare_code(bits[i], cfg, W, "c%d" % i) for i in range(len(bits))]
+    for i, (s0, c) in enumerate(zip(starts, codes)):
+        d, u = ref.demodulate_window(iq[2 * s0:2 * (s0 + W)], s0, cfg)
+        want = s.detect(d, u, [idx[c]], 0.25, s0, fs)
+        xc = s.batch_xcorr(d, [idx[c]])
+        want["code_index"] = c
+
+        def tie_ok(g, w, xc=xc):
+            return near_tie_margin(xc[0], int(w["peak_index"]), int(g["peak_index"])) < 1e-5
+
+        bad = compare_detections(dets[i:i + 1], want, fs, tie_ok=tie_ok, xc_ref={c: xc[0]}, eps=1e-5)
+        assert not bad, (i, bad)
+        assert int(dets[i]["window_start"]) == s0 and int(dets[i]["code_index"]) == c
+    assert dets[0]["accepted"] and dets[1]["accepted"] and dets[2]["accepted"]
+    assert not dets[3]["accepted"] and not dets[5]["accepted"]
+
+
+def test_tracking_rejects_bad_tasks(gpu_ctx):
+    from paper_2005_10445_b200 import capi
+    from paper_2005_10445_b200._abi import desk_config
+    cfg = desk_config(1024)
+    W = 1024 * 8 + 500
+    bits = np.random.default_rng(0).integers(0, 2, (2, 1024), dtype=np.uint8)
+    cs = capi.CodeSet.prepare(gpu_ctx, cfg, W, bits)
+    iq = np.zeros(2 * (W + 100), np.int16)
+    with pytest.raises(capi.InvalidArgument):
+        capi.track(gpu_ctx, cfg, iq, [200], [0], cs)          # window past the block
+    with pytest.raises(capi.InvalidArgument):
+        capi.track(gpu_ctx, cfg, iq, [0], [2], cs)            # code index out of range
+    assert capi.track(gpu_ctx, cfg, iq, [], [], cs).size == 0

@@ -26,6 +26,8 @@ ncu)
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_corr_pass --profile-from-start off -c 2 \
       -o $OUT/corr python bench.py --steps 1 --warmup 3 --no-cpu-baseline --profile-step > $OUT/ncuA.log 2>&1
   true ;;
+track)
+  timeout 600 python bench.py --workload tracking > $OUT/track.json 2> $OUT/track.err; echo "track rc=$?" >> $OUT/track.err ;;
 sweep)
   timeout 600 python tools/sweep.py $SWEEP > $OUT/sweep.log 2>&1 ;;
 esac
