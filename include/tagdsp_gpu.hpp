@@ -315,4 +315,31 @@ inline std::vector<tdg_detection> search(const RawSampleBlock& stream, const Win
     return out;
 }
 
+// Batched tracking (the Tracking branch of simulate_recording,
+// recording.cpp:360-378, for many scheduler Tasks at once): task i searches
+// window [starts[i], starts[i] + shape.window_len) of `stream` for code
+// codes[i] (prepared with prepare_code(code, shape, ...)).  One Detection per
+// task, accepted or not, as detect() returns for a single code.
+inline std::vector<Detection> track(const RawSampleBlock& stream, const WindowShape& shape,
+                                    std::span<const int64_t> starts, std::span<const TransformedCode* const> codes,
+                                    float threshold, PlanCache& cache) {
+    std::vector<Detection> out;
+    if (starts.size() != codes.size()) throw std::invalid_argument("track: one code per task");
+    if (codes.empty()) return out;
+    CodeCache& code_cache = *codes.front()->owner;
+    for (auto* tc : codes)
+        if (tc->window_len != shape.window_len || tc->owner != &code_cache)
+            throw std::invalid_argument("batch_xcorr: mixed window shapes");
+    tdg_codeset* set = code_cache.build(cache, shape.window_len);
+    std::vector<tdg_track_task> tasks(codes.size());
+    for (size_t i = 0; i < codes.size(); ++i) tasks[i] = {starts[i], codes[i]->index};
+    std::vector<tdg_detection> recs(tasks.size());
+    const tdg_demod_config c = shape.cfg.c();
+    detail::check(tdg_track(cache.handle(), &c, stream.samples.data(), stream.num_complex(), stream.start_time,
+                            tasks.data(), tasks.size(), set, threshold, recs.data()));
+    out.reserve(recs.size());
+    for (size_t i = 0; i < recs.size(); ++i) out.push_back(detail::to_detection(recs[i], codes[i]->tag_id));
+    return out;
+}
+
 }  // namespace tagdsp_gpu
