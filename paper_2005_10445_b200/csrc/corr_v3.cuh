@@ -38,6 +38,7 @@ __host__ __device__ constexpr int passb_row(int q) {
                                       : q * kTileB + 12 - ((q * kTileB) % 16) + ((q * kTileB) % 16 > 12 ? 16 : 0);
 }
 __host__ __device__ constexpr int even_up(int x) { return (x + 1) & ~1; }
+__host__ __device__ constexpr int up16(int x) { return (x + 15) & ~15; }   // float2 units: 128 bytes
 
 // Inter-pass twiddle table row stride (float2): row k1 holds
 // [w_N^{+k1 c}, c < QA][w_N^{+k1 QA e}, e < PA], padded to a 16-byte multiple.
@@ -49,18 +50,22 @@ struct Fused {
     static constexpr int QSA = qstride_even_pad(QA);
     static constexpr int TWS = inter_tw_stride(PA, QA);
     // pass-A slot: [D column][X columns: 2 per pair][transpose reuses D/X] [2 twiddle rows]
-    static constexpr int A_OPS = even_up(cmax((1 + 2 * kGroup) * LA, kGroup * 2 * PA * QSA));
-    static constexpr int A_SLOT = A_OPS + 2 * TWS;
+    // per-warp transpose / M staging region (128-byte aligned for the TMA store)
+    static constexpr int STG = up16(cmax(PA * QSA, LA));
+    static constexpr int A_OPS = up16(cmax((1 + 2 * kGroup) * LA, kGroup * 2 * STG));
+    static constexpr int A_SLOT = up16(A_OPS + 2 * TWS);
     static constexpr int ROWB = passb_row(QB);
-    static constexpr int B_SLOT = even_up(cmax(LB * kTileB, PB * ROWB));
+    static constexpr int B_SLOT = up16(cmax(LB * kTileB, PB * ROWB));
     static constexpr int SLOT = cmax(A_SLOT, B_SLOT);
     static constexpr int NT = 128;
     static constexpr size_t SMEM = 128 + 2 * size_t(SLOT) * 8;
     static_assert(cmax(PA, QA) <= 32 && cmax(PB, QB) <= 32, "one warp per column role");
+    static_assert(LA % kTileB == 0, "M tiles cover the t2 columns exactly (TMA store box)");
     static_assert(kTileB * cmax(PB, QB) <= NT, "pass-B tasks fit the CTA");
 };
 
 struct CorrSched {                     // one wave
+    CUtensorMap mstore;                // M ring as [pair][tile][k1][8 floats]: pass A's TMA stores
     const CorrGroup<kGroup>* groups;   // [ngw]
     const CorrPairOut* outs;           // [wave_pairs]
     const float2* twA;                 // w_{N2}^{+ac}, index a*QA + c
@@ -188,7 +193,7 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Ticket& k, 
     }
     __syncthreads();  // operands consumed
     if (act1) {
-        float2* tr = sl + role * P * QS + lane * QS;
+        float2* tr = sl + role * F::STG + lane * QS;
 #pragma unroll
         for (int c = 0; c < Q; ++c) tr[c] = v[c];
     }
@@ -196,7 +201,7 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Ticket& k, 
     // ---- step 2: lane c: twiddle, P-point IDFT over a, inter-pass twiddle, store M
     if (act && lane < Q) {
         const int c = lane;
-        const float2* tr = sl + role * P * QS + c;
+        const float2* tr = sl + role * F::STG + c;
         float2 w[P];
 #pragma unroll
         for (int a = 0; a < P; ++a) {
@@ -204,18 +209,22 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Ticket& k, 
             w[a] = a == 0 ? x : cmul(x, __ldg(&S.twA[a * Q + c]));
         }
         dft<P, +1>(w);
-        const int k1 = col ? N1 - cp : cp;
         const float2* twr = sl + F::A_OPS + col * TWS;
         const float2 tc = twr[c];
-        float2* M = gd.M[g] + size_t(k1) * kTileB + (c % kTileB) + size_t(c / kTileB) * N1 * kTileB;
+        // stage the column in t2 order in the warp's own region, then one TMA
+        // tensor store scatters it into M's tile-major layout (N2/4 chunks of
+        // 32 bytes) without occupying the LSU pipe
+        float2* stg = sl + role * F::STG;
+        __syncwarp(0xffffffffu >> (32 - Q));   // the region's transposed inputs are consumed
 #pragma unroll
-        for (int e = 0; e < P; ++e) {
-            const int t2 = c + Q * e;
-            const float2 tt = cmul(tc, twr[Q + e]);
-            if (Q % kTileB == 0)
-                M[size_t(Q / kTileB) * e * N1 * kTileB] = cmul(w[e], tt);
-            else
-                gd.M[g][(size_t(t2 / kTileB) * N1 + k1) * kTileB + (t2 % kTileB)] = cmul(w[e], tt);
+        for (int e = 0; e < P; ++e) stg[c + Q * e] = cmul(w[e], cmul(tc, twr[Q + e]));
+    }
+    if (act) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            tma_store_4d(&S.mstore, sl + role * F::STG, 0, col ? N1 - cp : cp, 0, gd.Mi[g]);
+            bulk_commit();
         }
     }
 }
@@ -323,7 +332,7 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Ticket& k, 
 // items with a 2-slot TMA ring (item i+1's bulk copies in flight while item i
 // computes).
 template <int PA, int QA, int PB, int QB, int TYPE>
-__global__ void __launch_bounds__(128, 3) k_corr_pass(const CorrSched S) {
+__global__ void __launch_bounds__(128, 3) k_corr_pass(const __grid_constant__ CorrSched S) {
     using F = Fused<PA, QA, PB, QB>;
     extern __shared__ __align__(128) unsigned char smraw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smraw);
@@ -364,8 +373,10 @@ __global__ void __launch_bounds__(128, 3) k_corr_pass(const CorrSched S) {
                 for (int l = threadIdx.x; l < F::LB * kTileB * 8 / 128; l += F::NT) discard_l2(tile + size_t(l) * 128);
             item_passB<PA, QA, PB, QB>(S, k, sl);
         }
+        if (TYPE == 0 && (threadIdx.x & 31) == 0) bulk_wait_read_all();   // staged M read by the TMA engine
         __syncthreads();   // slot s free for the prefetch of item + 2
     }
+    if (TYPE == 0 && (threadIdx.x & 31) == 0) bulk_wait_all();
 }
 
 }  // namespace tdg

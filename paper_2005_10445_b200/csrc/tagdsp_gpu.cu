@@ -10,6 +10,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <stdexcept>
@@ -19,6 +20,7 @@
 #include "tagdsp_gpu.h"
 #include "kernels.cuh"
 #include "corr_v3.cuh"
+#include <cudaTypedefs.h>
 
 namespace {
 
@@ -686,6 +688,35 @@ struct CorrJob {
     float* xc_b;
 };
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q{};
+        void* p = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !p) fail(TDG_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// The M ring as a 4-D fp32 tensor [pair][tile t2/4][k1][t2%4 as 8 floats]:
+// one pass-A TMA store writes a whole column k1 (box 8 x 1 x n_tiles x 1).
+CUtensorMap m_store_map(float2* M, int N1, int n_tiles, uint64_t Mstride, int n_pairs) {
+    CUtensorMap map;
+    const cuuint64_t dims[4] = {8, cuuint64_t(N1), cuuint64_t(n_tiles), cuuint64_t(n_pairs)};
+    const cuuint64_t strides[3] = {32, cuuint64_t(N1) * 32, Mstride * 8};
+    const cuuint32_t box[4] = {8, 1, cuuint32_t(n_tiles), 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    if (n_tiles > 256) fail(TDG_ERANGE, "M tile count %d exceeds a TMA box", n_tiles);
+    const CUresult r = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, M, dims, strides, box, estr,
+                                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(TDG_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+    return map;
+}
+
 // Waves of wave_pairs pairs; pass A of wave w on the context stream, pass B
 // on the second stream, M in a ring of `ring` wave buffers: B(w) waits for
 // A(w), A(w) waits for B(w - ring).  Pass B of wave w thus overlaps pass A of
@@ -720,6 +751,7 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
             g.Ca[g.npairs] = cs->spec.as<float2>() + jb.pair * N;
             g.Cb[g.npairs] = nullptr;
             g.M[g.npairs] = ctx->M.as<float2>() + (size_t(wv % ring) * wave + size_t(i)) * Mstride;
+            g.Mi[g.npairs] = (wv % ring) * wave + i;
             ++g.npairs;
         }
         ngw = std::max(ngw, int(gs.size()));
@@ -743,6 +775,7 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
     const size_t oo = ctx->pk_corr.add(outs);
     ctx->pk_corr.commit(ctx->stream);
     tdg::CorrSched S{};
+    S.mstore = m_store_map(ctx->M.as<float2>(), N1, n_tiles, Mstride, ring * wave);
     S.twA = ctx->twiddles(N2);
     S.twB = ctx->twiddles(N1);
     S.twI = ctx->inter_twiddles(N1, N2);
@@ -760,7 +793,6 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
     auto* gd = ctx->pk_corr.at<tdg::CorrGroup<G>>(og);
     auto* od = ctx->pk_corr.at<tdg::CorrPairOut>(oo);
     ctx->ensure_pipeline(ring);
-    KScope ks(ctx, "corr");   // spans both streams: the B stream joins back below
     CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
     CK(cudaStreamWaitEvent(ctx->stream_b, ctx->ev_fork, 0));
     for (int wv = 0; wv < n_waves; ++wv) {
@@ -1167,7 +1199,7 @@ void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float thre
     if (cs->window_len != w->W) fail(TDG_EINVAL, "batch_xcorr: mixed window shapes");
     for (uint64_t i = 0; i < cs->n_codes; ++i)
         if (w->W + cs->nlen[i] > cs->corr_len() + 1) fail(TDG_EINVAL, "batch_xcorr: window does not fit transform size");
-    const uint64_t ns = w->slots(), nc = cs->n_codes;
+    const uint64_t ns = w->used(), nc = cs->n_codes;
     ctx->keys.ensure(ns * nc * sizeof(unsigned long long));
     CK(cudaMemsetAsync(ctx->keys.p, 0, ns * nc * sizeof(unsigned long long), ctx->stream));
     std::vector<CorrJob> jobs;
@@ -1175,13 +1207,15 @@ void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float thre
     // code-pair-major: a group of kGroup stored pairs (whose spectra stay
     // L2-resident) sweeps every window slot before the next group starts
     const uint64_t npairs = (nc + 1) / 2, G = tdg::kGroup;
-    for (uint64_t p0 = 0; p0 < npairs; p0 += G)
+    for (uint64_t p0 = 0; p0 < npairs; p0 += G) {
         for (uint64_t s = 0; s < ns; ++s)
             for (uint64_t p = p0; p < std::min(npairs, p0 + G); ++p)
                 jobs.push_back({s, p, keys + s * nc + 2 * p, 2 * p + 1 < nc ? keys + s * nc + 2 * p + 1 : nullptr,
                                 nullptr, nullptr});
-    run_correlations(ctx, w, cs, jobs, false);
+    }
     ctx->det_dev.ensure(ns * nc * sizeof(tdg_detection));
+    // statistics: one CTA per (slot, code), slot-major so a window's d,u stay
+    // in L2 across all codes
     std::vector<tdg::StatsDesc> sd(ns * nc);
     for (uint64_t s = 0; s < ns; ++s)
         for (uint64_t c = 0; c < nc; ++c) {
@@ -1189,7 +1223,7 @@ void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float thre
             x.d = w->d.as<float>() + s * w->W;
             x.u = w->u.as<float>() + s * w->W;
             x.dc = cs->rep.as<float>() + c * cs->rep_cap;
-            x.key = ctx->keys.as<unsigned long long>() + s * nc + c;
+            x.key = keys + s * nc + c;
             x.out = ctx->det_dev.as<tdg_detection>() + s * nc + c;
             x.nonzero_len = uint32_t(cs->nlen[c]);
             x.energy = cs->energy[c];
@@ -1198,8 +1232,16 @@ void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float thre
             x.bin = int32_t(s % w->n_bins);
         }
     auto* sdd = ctx->upload(ctx->pk_misc, sd);
+    ensure_dspec(ctx, w, cs->N1, cs->N2);   // forward transforms (timed as fwd_pass1/2)
+    {
+        KScope ks(ctx, "corr");
+        run_correlations(ctx, w, cs, jobs, false);
+    }
+    // (running each finished code group's statistics under later waves on the
+    // second stream was measured slower: it delays the pass-B launches queued
+    // behind it and takes SM slots from the persistent passes)
     KScope ks(ctx, "stats");
-    tdg::k_stats<<<unsigned(ns * nc), 256, 0, ctx->stream>>>(sdd, uint32_t(w->W), fs, threshold);
+    tdg::k_stats<<<unsigned(sd.size()), 256, 0, ctx->stream>>>(sdd, uint32_t(w->W), fs, threshold);
     LAUNCHED();
     if (out) {
         CK(cudaMemcpyAsync(out, ctx->det_dev.p, ns * nc * sizeof(tdg_detection), cudaMemcpyDeviceToHost, ctx->stream));
