@@ -1,5 +1,5 @@
 """Execute the generated CUDA codelets (csrc/codelets.cuh, packed f32x2
-form written by tools/gen_codelets2.py) on the CPU by translating their
+form written by tools/gen_codelets.py) on the CPU by translating their
 straight-line bodies to Python, and compare with a float64 DFT.
 
 A packed value (64-bit register pair, lo = re, hi = im) is modelled as a

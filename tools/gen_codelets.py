@@ -1,37 +1,30 @@
 #!/usr/bin/env python3
-"""Generate straight-line register DFT codelets for the B200 FFT kernels.
+"""Generate PACKED-FP32 register DFT codelets for the B200 FFT kernels.
 
 Writes paper_2005_10445_b200/csrc/codelets.cuh: for every size R in SIZES and
 both directions, a fully unrolled `dft<R, SIGN>(float2 (&x)[R])` computing
     X[k] = sum_j x[j] * exp(SIGN * 2*pi*i*j*k/R)      (unnormalised)
-in place, in natural order.  Composite sizes use mixed-radix decimation in
-time (radix 4 first, then 2, 3, 5, 7); odd primes use the symmetric
-(x_j +/- x_{R-j}) form; twiddles are compile-time constants computed in
-double and rounded once to float, with the trivial ones (1, -1, +-i,
-(+-1 +-i)/sqrt2) special-cased so no multiply is spent on them.
+in place, in natural order.
+
+Every complex value is one 64-bit register pair and every operation is one
+sm_100a packed instruction (PTX add/sub/mul/fma .rn.f32x2 -> SASS FADD2 /
+FMUL2 / FFMA2), so a complex add costs one issue slot instead of two.
+Multiplications by +-1 and +-i are kept lazy (a quarter-turn count carried
+with each value) and folded into the next add/sub, where the swap of the
+real/imaginary halves is free (SASS operand selector .F32x2.LO_HI) and the
+signs come from a constant pair; a general complex constant costs FMUL2 +
+FFMA2.  Composite sizes use mixed-radix decimation in time (radix 4 first,
+then 2, 3, 5, 7); odd primes use the symmetric (x_j +/- x_{R-j}) form;
+constants are computed in double and rounded once to float.
 
 This is the B200 replacement for the per-stage butterflies FFTW executes
-inside fftwf_execute (reference proj/src/fft.cpp:51,62); the codelets run
-entirely in registers, so a CTA-level FFT of length P*Q needs only one
-shared-memory exchange.
+inside fftwf_execute (reference proj/src/fft.cpp:51,62).
 """
 import math
 import os
 import sys
 
 SIZES = [2, 3, 4, 5, 6, 7, 8, 9, 10, 12, 14, 15, 16, 18, 20, 21, 24, 25, 27, 28, 30, 32, 35, 36]
-
-
-class Em:
-    def __init__(self):
-        self.lines = []
-        self.n = 0
-
-    def tmp(self, expr):
-        self.n += 1
-        name = f"v{self.n}"
-        self.lines.append(f"    const float {name} = {expr};")
-        return name
 
 
 def lit(v):
@@ -41,37 +34,80 @@ def lit(v):
     return s + "f"
 
 
-def neg(a):
-    return a[1:] if a.startswith("-") else "-" + a
+def pair(a, b):
+    return f"pk({lit(a)}, {lit(b)})"
 
 
-def add(e, a, b):
-    if b.startswith("-"):
-        return e.tmp(f"{a} - {b[1:]}")
-    if a.startswith("-"):
-        return e.tmp(f"{b} - {a[1:]}")
-    return e.tmp(f"{a} + {b}")
+class Em:
+    def __init__(self):
+        self.lines = []
+        self.n = 0
+        self.ops = 0
+
+    def tmp(self, expr, op=True):
+        self.n += 1
+        name = f"v{self.n}"
+        self.lines.append(f"    const c2 {name} = {expr};")
+        if op:
+            self.ops += 1
+        return name
 
 
-def sub(e, a, b):
-    return add(e, a, neg(b))
-
-
-def cadd(e, a, b):
-    return (add(e, a[0], b[0]), add(e, a[1], b[1]))
-
-
-def csub(e, a, b):
-    return (sub(e, a[0], b[0]), sub(e, a[1], b[1]))
+# A complex value: (var, q) meaning var * i^q, q in 0..3.
+def rot(a, k):
+    return (a[0], (a[1] + k) % 4)
 
 
 def cneg(a):
-    return (neg(a[0]), neg(a[1]))
+    return rot(a, 2)
 
 
 def cmul_i(a, s):
-    # multiply by s*i (s = +1 or -1): (re, im) -> (-s*im, s*re)
-    return (neg(a[1]) if s > 0 else a[1], a[0] if s > 0 else neg(a[0]))
+    return rot(a, 1 if s > 0 else 3)
+
+
+def add_rel(e, x, y, q):
+    """x + y * i^q for plain vars x, y (one instruction)."""
+    if q == 0:
+        return e.tmp(f"add2({x}, {y})")
+    if q == 2:
+        return e.tmp(f"sub2({x}, {y})")
+    if q == 1:   # x + i y = (x.re - y.im, x.im + y.re)
+        return e.tmp(f"fma2(swp({y}), {pair(-1.0, 1.0)}, {x})")
+    return e.tmp(f"fma2(swp({y}), {pair(1.0, -1.0)}, {x})")   # x - i y
+
+
+def cadd(e, a, b):
+    # a + b = i^qa (A + B i^(qb - qa))
+    return (add_rel(e, a[0], b[0], (b[1] - a[1]) % 4), a[1])
+
+
+def csub(e, a, b):
+    return cadd(e, a, cneg(b))
+
+
+def cmul_c(e, a, c, s):
+    """a * (c + i s) for a general constant (quarter turns folded in)."""
+    z = complex(c, s) * (1j ** a[1])
+    c, s = z.real, z.imag
+    t = e.tmp(f"mul2({a[0]}, {pair(c, c)})")
+    return (e.tmp(f"fma2(swp({a[0]}), {pair(-s, s)}, {t})"), 0)
+
+
+def fma_real(e, acc, a, c):
+    """acc + a * c for a real constant c (one instruction)."""
+    if acc is None:
+        return (e.tmp(f"mul2({a[0]}, {pair(c, c)})"), a[1])
+    q = (a[1] - acc[1]) % 4
+    if q == 0:
+        v = e.tmp(f"fma2({a[0]}, {pair(c, c)}, {acc[0]})")
+    elif q == 2:
+        v = e.tmp(f"fma2({a[0]}, {pair(-c, -c)}, {acc[0]})")
+    elif q == 1:   # i a c = (-a.im c, a.re c)
+        v = e.tmp(f"fma2(swp({a[0]}), {pair(-c, c)}, {acc[0]})")
+    else:
+        v = e.tmp(f"fma2(swp({a[0]}), {pair(c, -c)}, {acc[0]})")
+    return (v, acc[1])
 
 
 def cmul_const(e, a, num, den, sign):
@@ -80,36 +116,10 @@ def cmul_const(e, a, num, den, sign):
     if num == 0:
         return a
     if (4 * num) % den == 0:
-        q = (4 * num) // den  # quarter turns
-        if q == 2:
-            return cneg(a)
-        return cmul_i(a, sign if q == 1 else -sign)
-    if (8 * num) % den == 0:
-        o = (8 * num) // den  # odd eighth turn: 1,3,5,7
-        h = lit(math.sqrt(0.5))
-        # exp(sign*i*pi*o/4) = (cx + i*sy)/sqrt2 with cx, sy in {+1, -1}
-        cx = 1 if o in (1, 7) else -1
-        sy = (1 if o in (1, 3) else -1) * sign
-        re, im = a
-        # (re + i im)(cx + i sy) = (cx re - sy im) + i (sy re + cx im)
-        r_re = e.tmp(f"({sgn(cx, re)} {'-' if sy > 0 else '+'} {par(im)}) * {h}")
-        r_im = e.tmp(f"({sgn(sy, re)} {'+' if cx > 0 else '-'} {par(im)}) * {h}")
-        return (r_re, r_im)
+        q = (4 * num) // den
+        return rot(a, (q * sign) % 4)
     ang = 2.0 * math.pi * num / den
-    c = math.cos(ang)
-    s = sign * math.sin(ang)
-    re, im = a
-    r_re = e.tmp(f"{par(re)} * {lit(c)} - {par(im)} * {lit(s)}")
-    r_im = e.tmp(f"{par(re)} * {lit(s)} + {par(im)} * {lit(c)}")
-    return (r_re, r_im)
-
-
-def sgn(s, x):
-    return par(x) if s > 0 else f"-{par(x)}"
-
-
-def par(x):
-    return f"({x})" if x.startswith("-") else x
+    return cmul_c(e, a, math.cos(ang), sign * math.sin(ang))
 
 
 def prime_dft(e, xs, sign):
@@ -124,7 +134,6 @@ def prime_dft(e, xs, sign):
         t2 = cadd(e, xs[1], xs[3])
         t3 = cmul_i(csub(e, xs[1], xs[3]), sign)
         return [cadd(e, t0, t2), cadd(e, t1, t3), csub(e, t0, t2), csub(e, t1, t3)]
-    # odd prime: symmetric form
     h = (r - 1) // 2
     A = [cadd(e, xs[j], xs[r - j]) for j in range(1, h + 1)]
     B = [csub(e, xs[j], xs[r - j]) for j in range(1, h + 1)]
@@ -135,24 +144,16 @@ def prime_dft(e, xs, sign):
     out = [None] * r
     out[0] = acc
     for k in range(1, h + 1):
-        pre, pim = x0
-        qre, qim = None, None
+        p = x0
+        qv = None
         for j in range(1, h + 1):
             c = math.cos(2.0 * math.pi * j * k / r)
             s = math.sin(2.0 * math.pi * j * k / r)
-            a = A[j - 1]
-            b = B[j - 1]
-            pre = e.tmp(f"{par(pre)} + {par(a[0])} * {lit(c)}")
-            pim = e.tmp(f"{par(pim)} + {par(a[1])} * {lit(c)}")
-            if qre is None:
-                qre = e.tmp(f"{par(b[0])} * {lit(s)}")
-                qim = e.tmp(f"{par(b[1])} * {lit(s)}")
-            else:
-                qre = e.tmp(f"{qre} + {par(b[0])} * {lit(s)}")
-                qim = e.tmp(f"{qim} + {par(b[1])} * {lit(s)}")
-        iq = cmul_i((qre, qim), sign)  # sign*i*Q
-        out[k] = cadd(e, (pre, pim), iq)
-        out[r - k] = csub(e, (pre, pim), iq)
+            p = fma_real(e, p, A[j - 1], c)
+            qv = fma_real(e, qv, B[j - 1], s)
+        iq = cmul_i(qv, sign)
+        out[k] = cadd(e, p, iq)
+        out[r - k] = csub(e, p, iq)
     return out
 
 
@@ -181,19 +182,68 @@ def dft(e, xs, sign):
     return out
 
 
+def materialize(e, a):
+    v, q = a
+    if q == 0:
+        return v
+    if q == 2:
+        return e.tmp(f"mul2({v}, {pair(-1.0, -1.0)})")
+    if q == 1:
+        return e.tmp(f"mul2(swp({v}), {pair(-1.0, 1.0)})")
+    return e.tmp(f"mul2(swp({v}), {pair(1.0, -1.0)})")
+
+
 def gen(n, sign):
     e = Em()
-    xs = []
-    for j in range(n):
-        xs.append((e.tmp(f"x[{j}].x"), e.tmp(f"x[{j}].y")))
+    xs = [(e.tmp(f"pk(x[{j}].x, x[{j}].y)", op=False), 0) for j in range(n)]
     out = dft(e, xs, sign)
+    outs = [materialize(e, o) for o in out]
     body = list(e.lines)
-    for k, (re, im) in enumerate(out):
-        body.append(f"    x[{k}] = make_float2({re}, {im});")
-    flops = sum(l.count("+") + l.count(" - ") + l.count("*") for l in e.lines)
-    head = f"// {n}-point DFT, sign {sign:+d}: {len(e.lines) - 2 * n} scalar ops (~{flops} flops)\n"
+    for k, v in enumerate(outs):
+        body.append(f"    x[{k}] = up({v});")
+    head = f"// {n}-point DFT, sign {sign:+d}: {e.ops} packed ops\n"
     head += f"template <> __device__ __forceinline__ void dft<{n}, {sign}>(float2 (&x)[{n}]) {{\n"
-    return head + "\n".join(body) + "\n}\n"
+    return head + "\n".join(body) + "\n}\n", e.ops
+
+
+HELPERS = r"""
+// Packed f32x2 helpers: a c2 is one 64-bit register pair (lo = re, hi = im).
+typedef unsigned long long c2;
+__device__ __forceinline__ c2 pk(float lo, float hi) {
+    c2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ float2 up(c2 v) {
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+    return r;
+}
+__device__ __forceinline__ c2 swp(c2 v) {   // (re, im) -> (im, re): a free operand selector in SASS
+    const float2 t = up(v);
+    return pk(t.y, t.x);
+}
+__device__ __forceinline__ c2 add2(c2 a, c2 b) {
+    c2 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ c2 sub2(c2 a, c2 b) {
+    c2 d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ c2 mul2(c2 a, c2 b) {
+    c2 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ c2 fma2(c2 a, c2 b, c2 c) {
+    c2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+"""
 
 
 def main():
@@ -201,16 +251,17 @@ def main():
         os.path.dirname(__file__), "..", "paper_2005_10445_b200", "csrc", "codelets.cuh")
     parts = [
         "// GENERATED by tools/gen_codelets.py -- do not edit.\n"
-        "// Straight-line register DFT codelets (see the generator docstring).\n"
+        "// Straight-line packed-FP32 register DFT codelets (see the generator docstring).\n"
         "#pragma once\n#include <cuda_runtime.h>\n\n"
-        "namespace tdg {\n\n"
+        "namespace tdg {\n" + HELPERS + "\n"
         "template <int R, int SIGN> __device__ __forceinline__ void dft(float2 (&x)[R]);\n\n"
         "template <> __device__ __forceinline__ void dft<1, -1>(float2 (&)[1]) {}\n"
         "template <> __device__ __forceinline__ void dft<1, 1>(float2 (&)[1]) {}\n\n"
     ]
     for n in SIZES:
         for sign in (-1, 1):
-            parts.append(gen(n, sign))
+            code, ops = gen(n, sign)
+            parts.append(code)
     parts.append("}  // namespace tdg\n")
     with open(out, "w") as f:
         f.write("\n".join(parts))
