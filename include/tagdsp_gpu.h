@@ -31,6 +31,7 @@ extern "C" {
 typedef struct tdg_ctx tdg_ctx;
 typedef struct tdg_codeset tdg_codeset;
 typedef struct tdg_windows tdg_windows;
+typedef struct tdg_ring tdg_ring;
 
 /* Message for the last failing call on this host thread. */
 const char* tdg_last_error(void);
@@ -145,6 +146,32 @@ int tdg_track(tdg_ctx* ctx, const tdg_demod_config* cfg, const int16_t* iq, uint
 int tdg_track_device(tdg_ctx* ctx, const tdg_demod_config* cfg, const int16_t* iq_dev, uint64_t n_complex,
                      int64_t stream_start, const tdg_track_task* tasks, uint64_t n_tasks,
                      const tdg_codeset* cs, float threshold, tdg_detection* out);
+
+/* Device-resident CircularBuffer (tagdsp::CircularBuffer,
+ * include/tagdsp/scheduler.hpp:11-40; proj/src/scheduler.cpp:7-45): the raw
+ * stream addressed by absolute sample index, same push (gap resync,
+ * eviction) and read semantics.  Pushes are asynchronous host->device copies
+ * on the ring's own stream; searches and tracking tasks read windows straight
+ * from the ring (no per-task copy, cf. the reference's read() into a vector)
+ * and a later push waits only for the reads whose slots it overwrites.
+ * Host buffers passed to push must stay valid until the copy completes
+ * (pinned memory: until a later synchronisation). */
+int tdg_ring_create(tdg_ctx* ctx, uint64_t capacity_samples, tdg_ring** out);
+void tdg_ring_destroy(tdg_ring* ring);
+int tdg_ring_push(tdg_ring* ring, const int16_t* iq, uint64_t n_complex, int64_t start,
+                  tdg_ring_push_result* result);
+int tdg_ring_read(tdg_ring* ring, int64_t start, int64_t end, int16_t* out, int* ok);
+int tdg_ring_bounds(const tdg_ring* ring, int64_t* head, int64_t* tail, uint64_t* capacity);
+/* Searching pass over n_windows windows [first_start + w*advance, + window_len)
+ * held by the ring (all bins x codes, records [window][bin][code]); sync = 0
+ * leaves the Detection copy-out in flight on the context stream
+ * (tdg_ctx_synchronize before reading `out`). */
+int tdg_search_ring(tdg_ctx* ctx, tdg_ring* ring, const tdg_demod_config* cfg, const double* lo_bins,
+                    uint64_t n_bins, int64_t first_start, uint64_t window_len, uint64_t advance,
+                    uint64_t n_windows, const tdg_codeset* cs, float threshold, tdg_detection* out,
+                    uint64_t out_cap, int sync);
+int tdg_track_ring(tdg_ctx* ctx, tdg_ring* ring, const tdg_demod_config* cfg, const tdg_track_task* tasks,
+                   uint64_t n_tasks, const tdg_codeset* cs, float threshold, tdg_detection* out, int sync);
 
 /* Tuning / profiling knobs (0 = default): "wave_pairs", "ring", "discard",
  * "fwd_wave", "one_stream", "cta_cap_a", "cta_cap_b",

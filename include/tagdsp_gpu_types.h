@@ -60,6 +60,14 @@ typedef struct tdg_track_task {
     uint64_t code_index;   /* code in the code set (prepared for the tracking window length) */
 } tdg_track_task;
 
+/* tagdsp::CircularBuffer::PushResult, include/tagdsp/scheduler.hpp:18-24 */
+typedef struct tdg_ring_push_result {
+    int64_t evicted_begin;
+    int64_t evicted_end;   /* == evicted_begin when nothing was evicted */
+    int32_t gap;           /* the block did not continue the stream: resynchronised */
+    int32_t reserved;
+} tdg_ring_push_result;
+
 /* Status codes of every C-ABI entry point (0 = ok).  The C++ wrapper maps
  * TDG_EINVAL to std::invalid_argument (the reference's precondition
  * exceptions) and everything else to std::runtime_error. */

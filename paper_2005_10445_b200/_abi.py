@@ -68,3 +68,9 @@ def composed_filter_len(cfg):
 
 # tdg_track_task (include/tagdsp_gpu_types.h)
 TRACK_TASK_DTYPE = np.dtype([("start", np.int64), ("code_index", np.uint64)])
+
+# tdg_ring_push_result (include/tagdsp_gpu_types.h)
+class RingPushResult(ctypes.Structure):
+    """tagdsp::CircularBuffer::PushResult (proj/include/tagdsp/scheduler.hpp:18-24)."""
+    _fields_ = [("evicted_begin", ctypes.c_int64), ("evicted_end", ctypes.c_int64), ("gap", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]

@@ -12,6 +12,8 @@ call raises.  Names and argument meaning follow the reference
   detect(ctx, windows, codes, threshold, fs)  detector.hpp:103-106
   search(ctx, cfg, bins, iq, ...)             recording.cpp:258-289 (detect_recording)
   track(ctx, cfg, iq, tasks, codes)           recording.cpp:360-378 (tracking tasks, batched)
+  Ring(ctx, capacity).push/read/bounds        scheduler.hpp:11-40 (CircularBuffer, device-resident)
+  search_ring / track_ring                    the same passes reading windows from a Ring
 
 Errors: TDG_EINVAL -> InvalidArgument (a ValueError, the reference's
 std::invalid_argument), anything else -> GpuError (RuntimeError).
@@ -21,7 +23,8 @@ import os
 
 import numpy as np
 
-from ._abi import DETECTION_DTYPE, TRACK_TASK_DTYPE, DemodConfig, demod_config, desk_config  # noqa: F401
+from ._abi import (DETECTION_DTYPE, TRACK_TASK_DTYPE, DemodConfig, RingPushResult, demod_config,  # noqa: F401
+                   desk_config)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtagdsp_gpu.so")
@@ -74,6 +77,15 @@ _PROTOS = {
                                  _P]),
     "tdg_track_device": (ctypes.c_int, [_P, ctypes.POINTER(DemodConfig), _P, _U64, _I64, _P, _U64, _P,
                                         ctypes.c_float, _P]),
+    "tdg_ring_create": (ctypes.c_int, [_P, _U64, ctypes.POINTER(_P)]),
+    "tdg_ring_destroy": (None, [_P]),
+    "tdg_ring_push": (ctypes.c_int, [_P, _P, _U64, _I64, ctypes.POINTER(RingPushResult)]),
+    "tdg_ring_read": (ctypes.c_int, [_P, _I64, _I64, _P, ctypes.POINTER(ctypes.c_int)]),
+    "tdg_ring_bounds": (ctypes.c_int, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64), ctypes.POINTER(_U64)]),
+    "tdg_search_ring": (ctypes.c_int, [_P, _P, ctypes.POINTER(DemodConfig), _P, _U64, _I64, _U64, _U64, _U64, _P,
+                                       ctypes.c_float, _P, _U64, ctypes.c_int]),
+    "tdg_track_ring": (ctypes.c_int, [_P, _P, ctypes.POINTER(DemodConfig), _P, _U64, _P, ctypes.c_float, _P,
+                                      ctypes.c_int]),
     "tdg_set_option": (ctypes.c_int, [_P, ctypes.c_char_p, _I64]),
     "tdg_kernel_time": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.POINTER(_U64), ctypes.POINTER(ctypes.c_double)]),
     "tdg_kernel_time_reset": (ctypes.c_int, [_P]),
@@ -349,4 +361,77 @@ def track(ctx, cfg, iq, starts, code_idx, codes, threshold=0.25, stream_start=0)
     out = np.zeros(tasks.size, dtype=DETECTION_DTYPE)
     _check(lib().tdg_track(ctx.handle, ctypes.byref(cfg), _ptr(iq), iq.size // 2, int(stream_start), _ptr(tasks),
                            tasks.size, codes._h, float(threshold), _ptr(out)))
+    return out
+
+
+class Ring:
+    """Device-resident CircularBuffer (proj/include/tagdsp/scheduler.hpp:11-40):
+    push(block, start) -> (evicted_begin, evicted_end, gap); read(start, end)
+    -> int16 I/Q or None if any part was evicted / not yet received."""
+
+    def __init__(self, ctx, capacity):
+        self.ctx = ctx
+        h = _P()
+        _check(lib().tdg_ring_create(ctx.handle, int(capacity), ctypes.byref(h)))
+        self._h = h
+        self._keep = []   # host blocks whose asynchronous upload may still be in flight
+
+    def push(self, iq, start):
+        iq = np.ascontiguousarray(iq, dtype=np.int16)
+        if iq.size % 2:
+            raise InvalidArgument("convert: odd raw sample count")
+        res = RingPushResult()
+        self._keep = self._keep[-3:] + [iq]
+        _check(lib().tdg_ring_push(self._h, _ptr(iq), iq.size // 2, int(start), ctypes.byref(res)))
+        return res.evicted_begin, res.evicted_end, bool(res.gap)
+
+    def read(self, start, end):
+        out = np.empty(2 * max(0, int(end) - int(start)), dtype=np.int16)
+        ok = ctypes.c_int()
+        _check(lib().tdg_ring_read(self._h, int(start), int(end), _ptr(out), ctypes.byref(ok)))
+        return out if ok.value else None
+
+    def bounds(self):
+        h, t, c = _I64(), _I64(), _U64()
+        _check(lib().tdg_ring_bounds(self._h, ctypes.byref(h), ctypes.byref(t), ctypes.byref(c)))
+        return h.value, t.value, c.value
+
+    @property
+    def head(self):
+        return self.bounds()[0]
+
+    @property
+    def tail(self):
+        return self.bounds()[1]
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tdg_ring_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def search_ring(ctx, ring, cfg, lo_bins, first_start, n_windows, codes, advance, threshold=0.25):
+    """Searching pass over windows [first_start + w*advance, + codes.window_len) held by `ring`."""
+    bins = np.ascontiguousarray(np.atleast_1d(lo_bins), dtype=np.float64)
+    out = np.zeros(int(n_windows) * bins.size * len(codes), dtype=DETECTION_DTYPE)
+    _check(lib().tdg_search_ring(ctx.handle, ring._h, ctypes.byref(cfg), _ptr(bins), bins.size, int(first_start),
+                                 codes.window_len, int(advance), int(n_windows), codes._h, float(threshold), _ptr(out),
+                                 out.size, 1))
+    return out
+
+
+def track_ring(ctx, ring, cfg, starts, code_idx, codes, threshold=0.25):
+    """Tracking tasks reading their windows from `ring` (see track())."""
+    tasks = np.zeros(len(starts), dtype=TRACK_TASK_DTYPE)
+    tasks["start"] = starts
+    tasks["code_index"] = code_idx
+    out = np.zeros(tasks.size, dtype=DETECTION_DTYPE)
+    _check(lib().tdg_track_ring(ctx.handle, ring._h, ctypes.byref(cfg), _ptr(tasks), tasks.size, codes._h,
+                                float(threshold), _ptr(out), 1))
     return out

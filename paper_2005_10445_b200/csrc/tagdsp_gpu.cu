@@ -623,7 +623,69 @@ struct tdg_windows {
     uint64_t used() const { return active ? active : slots(); }
 };
 
+// Device-resident CircularBuffer (include/tagdsp/scheduler.hpp:11-40,
+// proj/src/scheduler.cpp:7-45): the raw int16 I/Q stream addressed by
+// absolute sample index, sample t in slot t % cap.  Pushes are host->device
+// copies on the ring's own stream; compute on the context stream waits for
+// them through `pushed`, and each kernel that reads the ring registers its
+// sample range with an event, so a later push only waits for the reads whose
+// slots it overwrites (searches of second k overlap the upload of second k+1).
+struct tdg_ring {
+    tdg_ctx* ctx = nullptr;    // creating context (not owned)
+    int device = 0;
+    uint64_t cap = 0;          // complex samples
+    DevBuf buf;
+    int64_t head = 0, tail = 0;
+    cudaStream_t copy = nullptr;
+    cudaEvent_t pushed = nullptr;
+    struct Read {
+        int64_t s, e;
+        cudaEvent_t ev;
+    };
+    std::vector<Read> reads;
+    std::vector<cudaEvent_t> spare;
+    uint64_t slot(int64_t t) const {
+        const int64_t c = int64_t(cap);
+        return uint64_t(((t % c) + c) % c);
+    }
+    cudaEvent_t event() {
+        if (!spare.empty()) {
+            cudaEvent_t e = spare.back();
+            spare.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        return e;
+    }
+    // true if the sample ranges [a, a+na) and [b, b+nb) share a ring slot
+    bool overlap(int64_t a, uint64_t na, int64_t b, uint64_t nb) const {
+        if (!na || !nb) return false;
+        const uint64_t sa = slot(a), sb = slot(b);
+        return (sb + cap - sa) % cap < na || (sa + cap - sb) % cap < nb;
+    }
+};
+
 namespace {
+
+// Where a kernel's input samples live: a linear device block starting at
+// stream index `origin`, or the device ring (absolute-index slots).
+struct SampleSource {
+    const int16_t* base;
+    uint64_t len;
+    int64_t origin;
+    uint64_t ring_cap;
+    tdg_ring* ring;
+    static SampleSource linear(const int16_t* p, uint64_t n, int64_t start) { return {p, n, start, 0, nullptr}; }
+    static SampleSource of(tdg_ring* r) { return {r->buf.as<int16_t>(), r->cap, 0, r->cap, r}; }
+    bool holds(int64_t start, uint64_t n) const {
+        if (ring) return start >= ring->head && start + int64_t(n) <= ring->tail;
+        return start >= origin && uint64_t(start - origin) + n <= len;
+    }
+    uint64_t offset(int64_t start) const { return ring ? ring->slot(start) : uint64_t(start - origin); }
+    void before_read(tdg_ctx* ctx) const;
+    void after_read(tdg_ctx* ctx, int64_t s, int64_t e) const;
+};
 
 // Forward transforms of real sequences (pairs packed as r1 + i r2) into
 // Hermitian half-column spectra.
@@ -966,7 +1028,7 @@ void finish_codeset(tdg_ctx* ctx, tdg_codeset* cs, const float* d, const float* 
 
 void demod_launch(tdg_ctx* ctx, const void* in, bool int16_input, uint64_t in_len,
                   const std::vector<tdg::DemodWindowDesc>& wins, uint64_t W, int n_bins, uint64_t slot_stride,
-                  const float2* H, float eps) {
+                  const float2* H, float eps, uint64_t ring_cap = 0) {
     if (W == 0 || wins.empty()) return;
     const int V = 1024 - (ctx->clen - 1);
     const uint64_t nblocks = (W + uint64_t(V) - 1) / uint64_t(V);
@@ -978,11 +1040,11 @@ void demod_launch(tdg_ctx* ctx, const void* in, bool int16_input, uint64_t in_le
     if (int16_input) {
         set_smem(tdg::k_demod<int32_t, kDemodBlk>, sm);
         tdg::k_demod<int32_t, kDemodBlk><<<grid, kDemodBlk * 32, sm, ctx->stream>>>(
-            static_cast<const int32_t*>(in), in_len, wd, uint32_t(W), ctx->clen, n_bins, slot_stride, H, eps, tw);
+            static_cast<const int32_t*>(in), in_len, wd, uint32_t(W), ctx->clen, n_bins, slot_stride, H, eps, tw, ring_cap);
     } else {
         set_smem(tdg::k_demod<float2, kDemodBlk>, sm);
         tdg::k_demod<float2, kDemodBlk><<<grid, kDemodBlk * 32, sm, ctx->stream>>>(
-            static_cast<const float2*>(in), in_len, wd, uint32_t(W), ctx->clen, n_bins, slot_stride, H, eps, tw);
+            static_cast<const float2*>(in), in_len, wd, uint32_t(W), ctx->clen, n_bins, slot_stride, H, eps, tw, 0);
     }
     LAUNCHED();
 }
@@ -1127,23 +1189,36 @@ void tdg_windows_destroy(tdg_windows* w) {
 }
 
 namespace {
+void SampleSource::before_read(tdg_ctx* ctx) const {
+    if (ring) CK(cudaStreamWaitEvent(ctx->stream, ring->pushed, 0));
+}
+void SampleSource::after_read(tdg_ctx* ctx, int64_t s, int64_t e) const {
+    if (!ring) return;
+    cudaEvent_t ev = ring->event();
+    CK(cudaEventRecord(ev, ctx->stream));
+    ring->reads.push_back({s, e, ev});
+}
+
 void demodulate_impl(tdg_ctx* ctx, tdg_windows* win, const tdg_demod_config* cfg, const double* lo_bins,
-                     uint64_t n_bins, const int16_t* iq_dev, uint64_t n_complex, int64_t stream_start,
-                     uint64_t advance, uint64_t n_windows) {
+                     uint64_t n_bins, const SampleSource& src, int64_t first_start, uint64_t advance,
+                     uint64_t n_windows) {
     if (n_bins != win->n_bins) fail(TDG_EINVAL, "demodulate: bin count %llu != window set's %llu",
                                     (unsigned long long)n_bins, (unsigned long long)win->n_bins);
     if (n_windows > win->n_windows) fail(TDG_EINVAL, "demodulate: too many windows");
-    if (n_windows && (n_windows - 1) * advance + win->W > n_complex)
+    if (n_windows && !src.holds(first_start, (n_windows - 1) * advance + win->W))
         fail(TDG_EINVAL, "demodulate: windows exceed the sample block");
     std::vector<double> bins(lo_bins, lo_bins + n_bins);
     const float2* H = ctx->filter_spectra(*cfg, bins);
     std::vector<tdg::DemodWindowDesc> wins(n_windows);
     for (uint64_t w = 0; w < n_windows; ++w) {
         const uint64_t slot0 = w * n_bins;
-        wins[w] = {w * advance, win->d.as<float>() + slot0 * win->W, win->u.as<float>() + slot0 * win->W};
-        for (uint64_t b = 0; b < n_bins; ++b) win->start[slot0 + b] = stream_start + int64_t(w * advance);
+        const int64_t st = first_start + int64_t(w * advance);
+        wins[w] = {src.offset(st), win->d.as<float>() + slot0 * win->W, win->u.as<float>() + slot0 * win->W};
+        for (uint64_t b = 0; b < n_bins; ++b) win->start[slot0 + b] = st;
     }
-    demod_launch(ctx, iq_dev, true, n_complex, wins, win->W, int(n_bins), win->W, H, cfg->eps);
+    src.before_read(ctx);
+    demod_launch(ctx, src.base, true, src.len, wins, win->W, int(n_bins), win->W, H, cfg->eps, src.ring_cap);
+    if (n_windows) src.after_read(ctx, first_start, first_start + int64_t((n_windows - 1) * advance + win->W));
     win->dspec_N = 0;
 }
 }  // namespace
@@ -1153,7 +1228,8 @@ int tdg_demodulate_device(tdg_ctx* ctx, tdg_windows* win, const tdg_demod_config
                           uint64_t advance, uint64_t n_windows) {
     return guard([&] {
         CK(cudaSetDevice(ctx->device));
-        demodulate_impl(ctx, win, cfg, lo_bins, n_bins, iq_dev, n_complex, stream_start, advance, n_windows);
+        demodulate_impl(ctx, win, cfg, lo_bins, n_bins, SampleSource::linear(iq_dev, n_complex, stream_start),
+                        stream_start, advance, n_windows);
     });
 }
 
@@ -1164,8 +1240,9 @@ int tdg_demodulate(tdg_ctx* ctx, tdg_windows* win, const tdg_demod_config* cfg, 
         CK(cudaSetDevice(ctx->device));
         ctx->stream_buf.ensure(std::max<uint64_t>(n_complex, 1) * 2 * sizeof(int16_t));
         CK(cudaMemcpyAsync(ctx->stream_buf.p, iq, n_complex * 2 * sizeof(int16_t), cudaMemcpyHostToDevice, ctx->stream));
-        demodulate_impl(ctx, win, cfg, lo_bins, n_bins, ctx->stream_buf.as<int16_t>(), n_complex, stream_start, advance,
-                        n_windows);
+        demodulate_impl(ctx, win, cfg, lo_bins, n_bins,
+                        SampleSource::linear(ctx->stream_buf.as<int16_t>(), n_complex, stream_start), stream_start,
+                        advance, n_windows);
         CK(cudaStreamSynchronize(ctx->stream));
     });
 }
@@ -1195,7 +1272,8 @@ int tdg_windows_get_du(tdg_ctx* ctx, const tdg_windows* w, uint64_t slot, float*
 
 // ---- detection -------------------------------------------------------------
 namespace {
-void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float threshold, double fs, tdg_detection* out) {
+void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float threshold, double fs, tdg_detection* out,
+                 bool sync = true) {
     if (cs->window_len != w->W) fail(TDG_EINVAL, "batch_xcorr: mixed window shapes");
     for (uint64_t i = 0; i < cs->n_codes; ++i)
         if (w->W + cs->nlen[i] > cs->corr_len() + 1) fail(TDG_EINVAL, "batch_xcorr: window does not fit transform size");
@@ -1245,7 +1323,7 @@ void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float thre
     LAUNCHED();
     if (out) {
         CK(cudaMemcpyAsync(out, ctx->det_dev.p, ns * nc * sizeof(tdg_detection), cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
+        if (sync) CK(cudaStreamSynchronize(ctx->stream));
     }
 }
 }  // namespace
@@ -1304,8 +1382,9 @@ int tdg_search(tdg_ctx* ctx, const tdg_demod_config* cfg, const double* lo_bins,
         }
         ctx->stream_buf.ensure(n_complex * 2 * sizeof(int16_t));
         CK(cudaMemcpyAsync(ctx->stream_buf.p, iq, n_complex * 2 * sizeof(int16_t), cudaMemcpyHostToDevice, ctx->stream));
-        demodulate_impl(ctx, w, cfg, lo_bins, n_bins, ctx->stream_buf.as<int16_t>(), n_complex, stream_start, advance,
-                        n_windows);
+        demodulate_impl(ctx, w, cfg, lo_bins, n_bins,
+                        SampleSource::linear(ctx->stream_buf.as<int16_t>(), n_complex, stream_start), stream_start,
+                        advance, n_windows);
         detect_impl(ctx, w, cs, threshold, cfg->mod.sample_rate, out);
     });
 }
@@ -1319,14 +1398,13 @@ int tdg_search(tdg_ctx* ctx, const tdg_demod_config* cfg, const double* lo_bins,
 // windows, the forward transforms, one correlation job per task and one
 // statistics launch -- the latency-bound small batches of BASELINE configs[3].
 namespace {
-void track_impl(tdg_ctx* ctx, const tdg_demod_config* cfg, const int16_t* iq_dev, uint64_t n_complex,
-                int64_t stream_start, const tdg_track_task* tasks, uint64_t n_tasks, const tdg_codeset* cs,
-                float threshold, tdg_detection* out) {
+void track_impl(tdg_ctx* ctx, const tdg_demod_config* cfg, const SampleSource& src, const tdg_track_task* tasks,
+                uint64_t n_tasks, const tdg_codeset* cs, float threshold, tdg_detection* out, bool sync = true) {
     const uint64_t W = cs->window_len;
     for (uint64_t i = 0; i < n_tasks; ++i) {
         if (tasks[i].code_index >= cs->n_codes) fail(TDG_EINVAL, "track: task %llu code index out of range",
                                                      (unsigned long long)i);
-        if (tasks[i].start < stream_start || uint64_t(tasks[i].start - stream_start) + W > n_complex)
+        if (!src.holds(tasks[i].start, W))
             fail(TDG_EINVAL, "track: task %llu window outside the sample block", (unsigned long long)i);
         if (W + cs->nlen[tasks[i].code_index] > cs->corr_len() + 1)
             fail(TDG_EINVAL, "batch_xcorr: window does not fit transform size");
@@ -1346,10 +1424,19 @@ void track_impl(tdg_ctx* ctx, const tdg_demod_config* cfg, const int16_t* iq_dev
     const float2* H = ctx->filter_spectra(*cfg, bins);
     std::vector<tdg::DemodWindowDesc> wins(n_tasks);
     for (uint64_t i = 0; i < n_tasks; ++i) {
-        wins[i] = {uint64_t(tasks[i].start - stream_start), w->d.as<float>() + i * W, w->u.as<float>() + i * W};
+        wins[i] = {src.offset(tasks[i].start), w->d.as<float>() + i * W, w->u.as<float>() + i * W};
         w->start[i] = tasks[i].start;
     }
-    demod_launch(ctx, iq_dev, true, n_complex, wins, W, 1, W, H, cfg->eps);
+    src.before_read(ctx);
+    demod_launch(ctx, src.base, true, src.len, wins, W, 1, W, H, cfg->eps, src.ring_cap);
+    {
+        int64_t lo = tasks[0].start, hi = tasks[0].start;
+        for (uint64_t i = 0; i < n_tasks; ++i) {
+            lo = std::min(lo, tasks[i].start);
+            hi = std::max(hi, tasks[i].start);
+        }
+        src.after_read(ctx, lo, hi + int64_t(W));
+    }
     w->dspec_N = 0;
     // keys[i]: argmax of task i; keys[n_tasks]: sink for the stored pair's
     // other code (its correlation comes for free in the packed IFFT)
@@ -1388,7 +1475,7 @@ void track_impl(tdg_ctx* ctx, const tdg_demod_config* cfg, const int16_t* iq_dev
     if (out) {
         CK(cudaMemcpyAsync(out, ctx->det_dev.p, n_tasks * sizeof(tdg_detection), cudaMemcpyDeviceToHost,
                            ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
+        if (sync) CK(cudaStreamSynchronize(ctx->stream));
     }
 }
 }  // namespace
@@ -1399,7 +1486,7 @@ int tdg_track_device(tdg_ctx* ctx, const tdg_demod_config* cfg, const int16_t* i
     return guard([&] {
         CK(cudaSetDevice(ctx->device));
         if (n_tasks == 0) return;
-        track_impl(ctx, cfg, iq_dev, n_complex, stream_start, tasks, n_tasks, cs, threshold, out);
+        track_impl(ctx, cfg, SampleSource::linear(iq_dev, n_complex, stream_start), tasks, n_tasks, cs, threshold, out);
     });
 }
 
@@ -1412,8 +1499,167 @@ int tdg_track(tdg_ctx* ctx, const tdg_demod_config* cfg, const int16_t* iq, uint
         ctx->stream_buf.ensure(n_complex * 2 * sizeof(int16_t));
         CK(cudaMemcpyAsync(ctx->stream_buf.p, iq, n_complex * 2 * sizeof(int16_t), cudaMemcpyHostToDevice,
                            ctx->stream));
-        track_impl(ctx, cfg, ctx->stream_buf.as<int16_t>(), n_complex, stream_start, tasks, n_tasks, cs, threshold,
-                   out);
+        track_impl(ctx, cfg, SampleSource::linear(ctx->stream_buf.as<int16_t>(), n_complex, stream_start), tasks, n_tasks,
+                   cs, threshold, out);
+    });
+}
+
+
+// ---------------------------------------------------------------------------
+// Device-resident CircularBuffer and the searches/tracking tasks that read it.
+namespace {
+tdg_windows* search_windows(tdg_ctx* ctx, uint64_t window_len, uint64_t n_windows, uint64_t n_bins) {
+    tdg_windows* w = ctx->search_win;
+    if (!w || w->W != window_len || w->n_windows != n_windows || w->n_bins != n_bins) {
+        if (w) tdg_windows_destroy(w);
+        ctx->search_win = nullptr;
+        int rc = tdg_windows_create(ctx, window_len, n_windows, n_bins, &w);
+        if (rc) fail(rc, "%s", g_err.c_str());
+        ctx->search_win = w;
+    }
+    return w;
+}
+
+void ring_prune(tdg_ring* r) {
+    std::vector<tdg_ring::Read> keep;
+    for (auto& rd : r->reads) {
+        const cudaError_t q = cudaEventQuery(rd.ev);
+        if (q == cudaSuccess) {
+            r->spare.push_back(rd.ev);
+        } else if (q == cudaErrorNotReady) {
+            keep.push_back(rd);
+        } else {
+            CK(q);
+        }
+    }
+    r->reads.swap(keep);
+}
+}  // namespace
+
+int tdg_ring_create(tdg_ctx* ctx, uint64_t capacity, tdg_ring** out) {
+    return guard([&] {
+        *out = nullptr;
+        CK(cudaSetDevice(ctx->device));
+        if (capacity == 0) fail(TDG_EINVAL, "ring: capacity must be positive");
+        auto r = std::make_unique<tdg_ring>();
+        r->ctx = ctx;
+        r->device = ctx->device;
+        r->cap = capacity;
+        r->buf.ensure(capacity * 2 * sizeof(int16_t));
+        CK(cudaStreamCreateWithFlags(&r->copy, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&r->pushed, cudaEventDisableTiming));
+        CK(cudaMemsetAsync(r->buf.p, 0, r->buf.bytes, r->copy));
+        CK(cudaEventRecord(r->pushed, r->copy));
+        *out = r.release();
+    });
+}
+
+void tdg_ring_destroy(tdg_ring* r) {
+    if (!r) return;
+    cudaSetDevice(r->device);
+    cudaStreamSynchronize(r->copy);
+    for (auto& rd : r->reads) {
+        cudaEventSynchronize(rd.ev);
+        cudaEventDestroy(rd.ev);
+    }
+    for (auto e : r->spare) cudaEventDestroy(e);
+    if (r->pushed) cudaEventDestroy(r->pushed);
+    if (r->copy) cudaStreamDestroy(r->copy);
+    delete r;
+}
+
+int tdg_ring_bounds(const tdg_ring* r, int64_t* head, int64_t* tail, uint64_t* capacity) {
+    return guard([&] {
+        if (head) *head = r->head;
+        if (tail) *tail = r->tail;
+        if (capacity) *capacity = r->cap;
+    });
+}
+
+// CircularBuffer::push (proj/src/scheduler.cpp:11-33): same gap / eviction
+// bookkeeping; only the last `cap` samples of a block are uploaded.
+int tdg_ring_push(tdg_ring* r, const int16_t* iq, uint64_t n_complex, int64_t start, tdg_ring_push_result* res) {
+    return guard([&] {
+        CK(cudaSetDevice(r->device));
+        tdg_ring_push_result pr{};
+        if (start != r->tail) {   // gap in the stream: resynchronise at the new start
+            pr.gap = 1;
+            pr.evicted_begin = r->head;
+            pr.evicted_end = r->tail;
+            r->head = r->tail = start;
+        }
+        const uint64_t skip = n_complex > r->cap ? n_complex - r->cap : 0;
+        const int64_t t0 = start + int64_t(skip);
+        const uint64_t m = n_complex - skip;
+        if (m) {
+            ring_prune(r);
+            for (auto& rd : r->reads)
+                if (r->overlap(rd.s, uint64_t(rd.e - rd.s), t0, m)) CK(cudaStreamWaitEvent(r->copy, rd.ev, 0));
+            const uint64_t sl = r->slot(t0), first = std::min(m, r->cap - sl);
+            int16_t* dst = r->buf.as<int16_t>();
+            CK(cudaMemcpyAsync(dst + 2 * sl, iq + 2 * skip, first * 2 * sizeof(int16_t), cudaMemcpyHostToDevice,
+                               r->copy));
+            if (m > first)
+                CK(cudaMemcpyAsync(dst, iq + 2 * (skip + first), (m - first) * 2 * sizeof(int16_t),
+                                   cudaMemcpyHostToDevice, r->copy));
+            CK(cudaEventRecord(r->pushed, r->copy));
+        }
+        r->tail += int64_t(n_complex);
+        if (r->tail - r->head > int64_t(r->cap)) {
+            if (!pr.gap) {
+                pr.evicted_begin = r->head;
+                pr.evicted_end = r->tail - int64_t(r->cap);
+            }
+            r->head = r->tail - int64_t(r->cap);
+        }
+        if (res) *res = pr;
+    });
+}
+
+// CircularBuffer::read (proj/src/scheduler.cpp:35-45): *ok = 0 if any part
+// of [start, end) was evicted or not yet received.
+int tdg_ring_read(tdg_ring* r, int64_t start, int64_t end, int16_t* out, int* ok) {
+    return guard([&] {
+        CK(cudaSetDevice(r->device));
+        *ok = 0;
+        if (start < r->head || end > r->tail || start > end) return;
+        const uint64_t m = uint64_t(end - start);
+        if (m) {
+            const uint64_t sl = r->slot(start), first = std::min(m, r->cap - sl);
+            const int16_t* src = r->buf.as<int16_t>();
+            CK(cudaMemcpyAsync(out, src + 2 * sl, first * 2 * sizeof(int16_t), cudaMemcpyDeviceToHost, r->copy));
+            if (m > first)
+                CK(cudaMemcpyAsync(out + 2 * first, src, (m - first) * 2 * sizeof(int16_t), cudaMemcpyDeviceToHost,
+                                   r->copy));
+            CK(cudaStreamSynchronize(r->copy));
+        }
+        *ok = 1;
+    });
+}
+
+int tdg_search_ring(tdg_ctx* ctx, tdg_ring* r, const tdg_demod_config* cfg, const double* lo_bins, uint64_t n_bins,
+                    int64_t first_start, uint64_t window_len, uint64_t advance, uint64_t n_windows,
+                    const tdg_codeset* cs, float threshold, tdg_detection* out, uint64_t out_cap, int sync) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (advance == 0) fail(TDG_EINVAL, "search: advance must be positive");
+        if (n_windows == 0) return;
+        if (cs->window_len != window_len) fail(TDG_EINVAL, "batch_xcorr: mixed window shapes");
+        if (out && out_cap < n_windows * n_bins * cs->n_codes) fail(TDG_EINVAL, "search: output capacity too small");
+        if (r->device != ctx->device) fail(TDG_EINVAL, "search: ring and context on different devices");
+        tdg_windows* w = search_windows(ctx, window_len, n_windows, n_bins);
+        demodulate_impl(ctx, w, cfg, lo_bins, n_bins, SampleSource::of(r), first_start, advance, n_windows);
+        detect_impl(ctx, w, cs, threshold, cfg->mod.sample_rate, out, sync != 0);
+    });
+}
+
+int tdg_track_ring(tdg_ctx* ctx, tdg_ring* r, const tdg_demod_config* cfg, const tdg_track_task* tasks,
+                   uint64_t n_tasks, const tdg_codeset* cs, float threshold, tdg_detection* out, int sync) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (n_tasks == 0) return;
+        if (r->device != ctx->device) fail(TDG_EINVAL, "track: ring and context on different devices");
+        track_impl(ctx, cfg, SampleSource::of(r), tasks, n_tasks, cs, threshold, out, sync != 0);
     });
 }
 
