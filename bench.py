@@ -320,10 +320,21 @@ def main():
 
     nout = ctypes.c_uint64()
 
+    # end-to-end = the streaming public API: each step uploads one second of
+    # pinned host I/Q into the device-resident CircularBuffer (tdg_ring_push,
+    # its own copy stream) and searches that second's windows straight from
+    # the ring (tdg_search_ring), Detection records copied back to pinned host
+    # memory; the upload of second k+1 overlaps the search of second k.
+    ring = capi.Ring(ctx, 3 * n_complex)
+    stream_pos = [0]
+
     def step_e2e():
-        capi._check(lib.tdg_search(ctx.handle, ctypes.byref(cfg), capi._ptr(bins), bins.size,
-                                   ctypes.c_void_p(iq_pin.data_ptr()), n_complex, 0, W, ADV, cs._h, 0.25,
-                                   ctypes.c_void_p(out_pin.data_ptr()), n_units, ctypes.byref(nout)))
+        start = stream_pos[0]
+        capi._check(lib.tdg_ring_push(ring._h, ctypes.c_void_p(iq_pin.data_ptr()), n_complex, start, None))
+        capi._check(lib.tdg_search_ring(ctx.handle, ring._h, ctypes.byref(cfg), capi._ptr(bins), bins.size, start, W,
+                                        ADV, N_WIN, cs._h, 0.25, ctypes.c_void_p(out_pin.data_ptr()), n_units,
+                                        int(world > 1)))
+        stream_pos[0] += n_complex
         if world > 1:
             # the path's one exchange: every rank's accepted detections, all-gathered over NCCL
             from paper_2005_10445_b200 import dist as tdist
@@ -429,7 +440,9 @@ def main():
         "real_time_factor_e2e": (N_WIN * ADV / FS) / (e2e_ms / 1e3),
         "e2e": {"value": e2e, "unit": "corr/s", "ms_per_step": e2e_ms, "wall_ms_per_step": wall_ms,
                 "h2d_bytes_per_step": int(iq.nbytes), "d2h_bytes_per_step": int(n_units * DETECTION_DTYPE.itemsize),
-                "path": "tdg_search() C-ABI, pinned host int16 in, Detection records out"},
+                "path": "streaming C-ABI: tdg_ring_push (pinned host int16 -> device CircularBuffer, copy "
+                        "stream) + tdg_search_ring (Detection records -> pinned host), upload of step k+1 "
+                        "overlapping the search of step k"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm",
                      "kernel": "correlation engine per step: k_corr_pass<27,32,32,32,0> (spectral product + "
