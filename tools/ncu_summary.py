@@ -30,33 +30,45 @@ def ncu_csv(rep, page, *extra):
 
 
 def full(rep):
+    """One table per profiled launch: SOL / occupancy / launch / scheduler
+    sections, DRAM and instruction counters, and the stall breakdown."""
     rows = ncu_csv(rep, "details")
     h = rows[0]
-    kern = None
-    lines = []
+    per = collections.OrderedDict()   # launch ID -> (kernel, lines)
     for r in rows[1:]:
         d = dict(zip(h, r))
-        kern = kern or d.get("Kernel Name")
+        lid = d.get("ID")
+        if lid not in per:
+            per[lid] = (d.get("Kernel Name"), [])
         for sec, names in KEYS:
             if d.get("Section Name") == sec and d.get("Metric Name") in names:
-                lines.append("| %s | %s | %s %s |" % (sec.split()[0], d["Metric Name"], d["Metric Value"], d["Metric Unit"]))
+                per[lid][1].append("| %s | %s | %s %s |" % (sec.split()[0], d["Metric Name"], d["Metric Value"],
+                                                             d["Metric Unit"]))
     raw = ncu_csv(rep, "raw")
-    rh, units, rv = raw[0], raw[1], raw[2]
-    stalls = []
-    for name, u, v in zip(rh, units, rv):
-        if name in RAW:
-            lines.append("| raw | %s | %s %s |" % (name, v, u))
-        if name.startswith("smsp__average_warps_issue_stalled_") and name.endswith("_per_issue_active.ratio"):
-            try:
-                if float(v) >= 0.05:
-                    stalls.append((float(v), name[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
-            except ValueError:
-                pass
-    stalls.sort(reverse=True)
-    lines.append("| stalls | per issued instruction | %s |" % ", ".join("%s %.2f" % (n, v) for v, n in stalls))
-    print("### %s\n\n`%s`\n\n| section | metric | value |\n|---|---|---|" % (rep.split("/")[-1], kern))
-    print("\n".join(lines))
-    print()
+    rh, units = raw[0], raw[1]
+    for i, rv in enumerate(raw[2:]):
+        lid = list(per.keys())[i] if i < len(per) else None
+        if lid is None:
+            break
+        lines = per[lid][1]
+        stalls = []
+        for name, u, v in zip(rh, units, rv):
+            if name in RAW:
+                lines.append("| raw | %s | %s %s |" % (name, v, u))
+            if name.startswith("smsp__average_warps_issue_stalled_") and name.endswith("_per_issue_active.ratio"):
+                try:
+                    if float(v) >= 0.05:
+                        stalls.append((float(v), name[len("smsp__average_warps_issue_stalled_"):
+                                                      -len("_per_issue_active.ratio")]))
+                except ValueError:
+                    pass
+        stalls.sort(reverse=True)
+        lines.append("| stalls | per issued instruction | %s |" % ", ".join("%s %.2f" % (n, v) for v, n in stalls))
+    for lid, (kern, lines) in per.items():
+        print("### %s, launch %s\n\n`%s`\n\n| section | metric | value |\n|---|---|---|" % (rep.split("/")[-1], lid,
+                                                                                              kern))
+        print("\n".join(lines))
+        print()
 
 
 def launches(path, traffic_out=None):
