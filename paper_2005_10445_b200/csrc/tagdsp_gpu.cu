@@ -420,7 +420,7 @@ struct tdg_ctx {
     DevBuf hspec;
     int clen = 0;
     // scratch
-    DevBuf T, M, keys, det_dev, stream_buf;
+    DevBuf T, M, keys, det_dev, stream_buf, stats_part, stats_ctr;
     // second stream + events of the two-stream correlation pipeline
     cudaStream_t stream_b = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -783,6 +783,29 @@ CUtensorMap m_store_map(float2* M, int N1, int n_tiles, uint64_t Mstride, int n_
 // on the second stream, M in a ring of `ring` wave buffers: B(w) waits for
 // A(w), A(w) waits for B(w - ring).  Pass B of wave w thus overlaps pass A of
 // wave w+1 and neither kernel's ramp or tail leaves SMs idle.
+// statistics (k_stats): one CTA per (slot, code) when there are enough of
+// them to fill the GPU, else each dot product split over several CTAs
+void launch_stats(tdg_ctx* ctx, const tdg::StatsDesc* sd, size_t n, uint32_t W, double fs, float threshold) {
+    if (!n) return;
+    const size_t want = size_t(num_sms()) * 8;
+    int splits = n >= want ? 1 : int(std::min<size_t>(64, (want + n - 1) / n));
+    double* partial = nullptr;
+    unsigned* counters = nullptr;
+    if (splits > 1) {
+        ctx->stats_part.ensure(n * size_t(splits) * 5 * sizeof(double));
+        if (ctx->stats_ctr.bytes < n * sizeof(unsigned)) {
+            ctx->stats_ctr.ensure(n * sizeof(unsigned));
+            CK(cudaMemsetAsync(ctx->stats_ctr.p, 0, ctx->stats_ctr.bytes, ctx->stream));
+        }
+        partial = ctx->stats_part.as<double>();
+        counters = ctx->stats_ctr.as<unsigned>();
+    }
+    KScope ks(ctx, "stats");
+    tdg::k_stats<<<unsigned(n * size_t(splits)), 256, 0, ctx->stream>>>(sd, W, fs, threshold, splits, partial,
+                                                                       counters);
+    LAUNCHED();
+}
+
 void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const std::vector<CorrJob>& jobs,
                       bool write_xc) {
     if (jobs.empty()) return;
@@ -1318,9 +1341,7 @@ void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float thre
     // (running each finished code group's statistics under later waves on the
     // second stream was measured slower: it delays the pass-B launches queued
     // behind it and takes SM slots from the persistent passes)
-    KScope ks(ctx, "stats");
-    tdg::k_stats<<<unsigned(sd.size()), 256, 0, ctx->stream>>>(sdd, uint32_t(w->W), fs, threshold);
-    LAUNCHED();
+    launch_stats(ctx, sdd, sd.size(), uint32_t(w->W), fs, threshold);
     if (out) {
         CK(cudaMemcpyAsync(out, ctx->det_dev.p, ns * nc * sizeof(tdg_detection), cudaMemcpyDeviceToHost, ctx->stream));
         if (sync) CK(cudaStreamSynchronize(ctx->stream));
@@ -1467,11 +1488,7 @@ void track_impl(tdg_ctx* ctx, const tdg_demod_config* cfg, const SampleSource& s
         x.bin = 0;
     }
     auto* sdd = ctx->upload(ctx->pk_misc, sd);
-    {
-        KScope ks(ctx, "stats");
-        tdg::k_stats<<<unsigned(n_tasks), 256, 0, ctx->stream>>>(sdd, uint32_t(W), cfg->mod.sample_rate, threshold);
-        LAUNCHED();
-    }
+    launch_stats(ctx, sdd, n_tasks, uint32_t(W), cfg->mod.sample_rate, threshold);
     if (out) {
         CK(cudaMemcpyAsync(out, ctx->det_dev.p, n_tasks * sizeof(tdg_detection), cudaMemcpyDeviceToHost,
                            ctx->stream));
