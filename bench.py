@@ -138,10 +138,32 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
 
 
-def make_inputs(rank, world):
+# BASELINE.json configs: (codes per GPU, roster size, own stream per rank?)
+WORKLOADS = {
+    # configs[1]: 64 tag codes per GPU, tag set sharded, one shared stream
+    "search": dict(per_gpu=lambda world: N_CODES, roster=lambda world: N_CODES * world, own_stream=False,
+                   text="cfg2: %d tag codes/GPU x 1 s of 8 Ms/s int16 I/Q"),
+    # configs[2]: 1024 tag codes sharded across the GPUs, detections gathered
+    "roster": dict(per_gpu=lambda world: (1024 + world - 1) // world, roster=lambda world: 1024, own_stream=False,
+                   text="cfg3: 1024 tag codes sharded (%d per GPU) x 1 s of 8 Ms/s int16 I/Q"),
+    # configs[4]: one I/Q stream per GPU (multi-antenna), 256 codes each
+    "streams": dict(per_gpu=lambda world: 256, roster=lambda world: 256, own_stream=True,
+                    text="cfg5: one 8 Ms/s int16 I/Q stream per GPU x %d tag codes, 1 s"),
+}
+
+
+def make_inputs(rank, world, workload="search"):
+    """This rank's code bits, its stream, the injections and the roster index
+    of its first code."""
     from paper_2005_10445_b200 import synth
-    bits_all, iq, inj, truth = synth.cfg2_scene(n_codes=N_CODES * world, n_inject=16)
-    return bits_all[rank * N_CODES:(rank + 1) * N_CODES], iq, inj
+    wl = WORKLOADS[workload]
+    per, roster = wl["per_gpu"](world), wl["roster"](world)
+    seed = 7 + (rank if wl["own_stream"] else 0)
+    bits_all, iq, inj, truth = synth.cfg2_scene(n_codes=roster, n_inject=16, seed=seed)
+    if wl["own_stream"]:
+        return bits_all, iq, inj, 0
+    lo = min(rank * per, roster)
+    return bits_all[lo:min(roster, lo + per)], iq, inj, lo
 
 
 def run_reference(args):
@@ -156,7 +178,7 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtagdsp_ref.so not built"}))
         return
     cfg = demod_config()
-    bits, iq, _ = make_inputs(0, 1)
+    bits, iq, _, _ = make_inputs(0, 1)
     threads = os.cpu_count() or 1
     n_codes = args.ref_codes
     # bounded sample: 1 window x all 9 bins x n_codes codes
@@ -183,13 +205,17 @@ def run_reference(args):
     print(json.dumps(line))
 
 
-def workload_config(world):
-    return {"workload": "cfg2: %d tag codes/GPU x 1 s of 8 Ms/s int16 I/Q (%d windows of %d, advance %d) x %d "
-                        "lo_freq bins (-400..+400 kHz)" % (N_CODES, N_WIN, W, ADV, len(BINS)),
-            "codes_per_gpu": N_CODES, "windows": N_WIN, "window_len": W, "bins": len(BINS), "corr_len": CORR_LEN,
-            "correlations_per_step_per_gpu": N_CODES * N_WIN * len(BINS),
+def workload_config(world, workload="search"):
+    wl = WORKLOADS[workload]
+    per = wl["per_gpu"](world)
+    return {"workload": (wl["text"] % per) + " (%d windows of %d, advance %d) x %d lo_freq bins (-400..+400 kHz)" % (
+                N_WIN, W, ADV, len(BINS)),
+            "codes_per_gpu": per, "roster": wl["roster"](world), "windows": N_WIN, "window_len": W,
+            "bins": len(BINS), "corr_len": CORR_LEN,
+            "correlations_per_step_per_gpu": per * N_WIN * len(BINS),
             "l2": "working set (223 MB code spectra + 345 MB window spectra) exceeds the 126 MB L2; no flush",
-            "parallelism": "tag-set sharding, %d GPU(s)" % world}
+            "parallelism": ("one stream per GPU, %d GPU(s)" if wl["own_stream"] else "tag-set sharding, %d GPU(s)") %
+                           world}
 
 
 def cpu_baseline_sample(bits, iq):
@@ -224,7 +250,7 @@ def run_tracking(args):
     from paper_2005_10445_b200._abi import DETECTION_DTYPE, TRACK_TASK_DTYPE, demod_config
     lib = capi.lib()
     cfg = demod_config()
-    bits, iq, inj = make_inputs(rank, world)
+    bits, iq, inj, _ = make_inputs(rank, world)
     TW, PRE = 96000, 16000
     n = iq.size // 2
     ctx = capi.Context(local)
@@ -273,8 +299,9 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="search", choices=["search", "tracking"],
-                    help="search: BASELINE configs[1] (the headline line); tracking: configs[3]")
+    ap.add_argument("--workload", default="search", choices=["search", "roster", "streams", "tracking"],
+                    help="search: BASELINE configs[1] (the headline line); roster: configs[2]; "
+                         "tracking: configs[3]; streams: configs[4]")
     ap.add_argument("--ref-codes", type=int, default=16)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-step", action="store_true",
@@ -300,7 +327,8 @@ def main():
     from paper_2005_10445_b200._abi import DETECTION_DTYPE, demod_config
     lib = capi.lib()
     cfg = demod_config()
-    bits, iq, inj = make_inputs(rank, world)
+    bits, iq, inj, code0 = make_inputs(rank, world, args.workload)
+    n_codes = len(bits)
     n_complex = iq.size // 2
     ctx = capi.Context(local)
     cs = capi.CodeSet.prepare(ctx, cfg, W, bits)
@@ -308,7 +336,7 @@ def main():
     win = capi.Windows(ctx, W, N_WIN, len(BINS))
     iq_dev = torch.from_numpy(iq).to(f"cuda:{local}")
     iq_pin = torch.from_numpy(iq).pin_memory()
-    n_units = N_CODES * N_WIN * len(BINS)
+    n_units = n_codes * N_WIN * len(BINS)
     out_pin = torch.empty(n_units * DETECTION_DTYPE.itemsize, dtype=torch.uint8).pin_memory()
     stream = torch.cuda.ExternalStream(ctx.stream(), device=f"cuda:{local}")
     bins = np.ascontiguousarray(BINS)
@@ -339,7 +367,7 @@ def main():
             # the path's one exchange: every rank's accepted detections, all-gathered over NCCL
             from paper_2005_10445_b200 import dist as tdist
             recs = np.frombuffer(out_pin.numpy().tobytes(), dtype=DETECTION_DTYPE)
-            tdist.gather_detections(recs, rank * N_CODES, device=f"cuda:{local}", accepted_only=True)
+            tdist.gather_detections(recs, code0, device=f"cuda:{local}", accepted_only=True)
 
     def barrier():
         torch.cuda.synchronize()
@@ -412,7 +440,7 @@ def main():
     pk = peaks()
     n_corr_launch, ms_corr = kt["corr"]
     corr_ms_step = ms_corr / max(1, n_corr_launch)
-    bpc = bytes_per_corr(len(BINS), N_CODES)
+    bpc = bytes_per_corr(len(BINS), n_codes)
     achieved = bpc * n_units / (corr_ms_step / 1e3) / 1e9
     total_ms = sum(v[1] for v in kt.values())
     shares = {k: round(v[1] / total_ms, 4) if total_ms else None for k, v in kt.items()}
@@ -433,7 +461,7 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (numpy scene: 16 of the codes injected at known fractional delays, offsets "
                 "U(-200,200) kHz, SNR {0,5,10,20} dB in 10 dB noise; int16 at scale 8192)",
-        "config": dict(workload_config(world), corr_len_b200=corr_len_used),
+        "config": dict(workload_config(world, args.workload), corr_len_b200=corr_len_used),
         # stream seconds searched per wall second for the whole roster (64 x
         # n_gpus codes) x 9 bins: N_WIN windows x advance per step
         "real_time_factor": (N_WIN * ADV / FS) / (ms_max / 1e3),
@@ -447,7 +475,7 @@ def main():
         "roofline": {"bound": "hbm",
                      "kernel": "correlation engine per step: k_corr_pass<27,32,32,32,0> (spectral product + "
                                "first inverse-FFT pass) and k_corr_pass<...,1> (second pass + argmax), "
-                               "%d launches on two overlapped streams" % (2 * ((N_CODES // 2 + 7) // 8) * N_WIN * len(BINS)),
+                               "%d launches on two overlapped streams" % (2 * (((n_codes + 1) // 2 * N_WIN * len(BINS) + 7) // 8)),
                      "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
                      "traffic": traffic, "peak_source": pk["source"],
                      "traffic_note": "dram__bytes_read+write of all correlation launches of one step, warm L2 "
