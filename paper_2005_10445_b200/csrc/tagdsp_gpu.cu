@@ -801,8 +801,11 @@ void launch_stats(tdg_ctx* ctx, const tdg::StatsDesc* sd, size_t n, uint32_t W, 
         counters = ctx->stats_ctr.as<unsigned>();
     }
     KScope ks(ctx, "stats");
-    tdg::k_stats<<<unsigned(n * size_t(splits)), 256, 0, ctx->stream>>>(sd, W, fs, threshold, splits, partial,
-                                                                       counters);
+    if (splits > 1)
+        tdg::k_stats<true><<<unsigned(n * size_t(splits)), 256, 0, ctx->stream>>>(sd, W, fs, threshold, splits,
+                                                                             partial, counters);
+    else
+        tdg::k_stats<false><<<unsigned(n), 256, 0, ctx->stream>>>(sd, W, fs, threshold, 1, nullptr, nullptr);
     LAUNCHED();
 }
 
@@ -1056,7 +1059,7 @@ void demod_launch(tdg_ctx* ctx, const void* in, bool int16_input, uint64_t in_le
     const int V = 1024 - (ctx->clen - 1);
     const uint64_t nblocks = (W + uint64_t(V) - 1) / uint64_t(V);
     dim3 grid(unsigned((nblocks + kDemodBlk - 1) / kDemodBlk), unsigned(wins.size()));
-    const size_t sm = size_t(kDemodBlk) * (1024 + 32 * 33) * sizeof(float2) + size_t(kDemodBlk) * 1024 * sizeof(float);
+    const size_t sm = size_t(kDemodBlk) * (32 * 33) * sizeof(float2) + size_t(kDemodBlk) * 1024 * sizeof(float);
     const float2* tw = ctx->twiddles(1024);
     auto* wd = ctx->upload(ctx->pk_misc, wins);
     KScope ks(ctx, "demod");
