@@ -12,6 +12,8 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <mutex>
+#include <tuple>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -251,7 +253,18 @@ bool choose_corr_len(uint64_t need, int* n1, int* n2) {
 // Kernel dispatch by pass length
 template <class T>
 void set_smem(T* kernel, size_t bytes) {
-    if (bytes > 48 * 1024) CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    // once per (kernel, size): the attribute call costs a few microseconds,
+    // which matters for latency-bound tracking batches
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, size_t, int>, bool> done;
+    if (bytes <= 48 * 1024) return;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), bytes, dev);
+    if (done.count(key)) return;
+    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
+    done[key] = true;
 }
 
 int block_for(int tasks) {
@@ -311,10 +324,25 @@ int num_sms() {
 
 template <class K>
 int persistent_grid(K* kernel, int threads, size_t smem, int n_items) {
-    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    CK(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    // attributes + occupancy once per (kernel, threads, smem) and device
+    static std::mutex mu;
+    static std::map<std::tuple<const void*, int, size_t, int>, int> cache;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    const auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), threads, smem, dev);
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            per_sm = it->second;
+        } else {
+            CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            CK(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+            cache[key] = per_sm;
+        }
+    }
     if (per_sm < 1) fail(TDG_ECUDA, "kernel does not fit on an SM (smem %zu)", smem);
     return std::max(1, std::min(n_items, per_sm * num_sms()));
 }

@@ -21,7 +21,7 @@ def main():
     B = int(sys.argv[1]) if len(sys.argv) > 1 else 1
     lib = capi.lib()
     cfg = demod_config()
-    bits, iq, inj = bench.make_inputs(0, 1)
+    bits, iq, inj, _ = bench.make_inputs(0, 1)
     n = iq.size // 2
     ctx = capi.Context(0)
     cs = capi.CodeSet.prepare(ctx, cfg, 96000, bits)
