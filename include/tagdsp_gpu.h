@@ -173,8 +173,8 @@ int tdg_search_ring(tdg_ctx* ctx, tdg_ring* ring, const tdg_demod_config* cfg, c
 int tdg_track_ring(tdg_ctx* ctx, tdg_ring* ring, const tdg_demod_config* cfg, const tdg_track_task* tasks,
                    uint64_t n_tasks, const tdg_codeset* cs, float threshold, tdg_detection* out, int sync);
 
-/* Tuning / profiling knobs (0 = default): "wave_pairs", "ring", "discard",
- * "fwd_wave", "one_stream", "cta_cap_a", "cta_cap_b",
+/* Tuning / profiling knobs (0 = default): "wave_pairs", "ring", "n_streams",
+ * "discard", "fwd_wave", "one_stream", "cta_cap_a", "cta_cap_b",
  * "time_kernels" (1 = record a CUDA event pair on the context stream around
  * every launch; read back with tdg_kernel_time). */
 int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value);

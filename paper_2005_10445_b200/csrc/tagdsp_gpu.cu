@@ -449,12 +449,24 @@ struct tdg_ctx {
     int clen = 0;
     // scratch
     DevBuf T, M, keys, det_dev, stream_buf, stats_part, stats_ctr;
-    // second stream + events of the two-stream correlation pipeline
-    cudaStream_t stream_b = nullptr;
+    // streams + events of the multi-stream correlation pipeline
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::vector<cudaEvent_t> ev_a, ev_b;
-    void ensure_pipeline(int ring) {
-        if (!stream_b) CK(cudaStreamCreateWithFlags(&stream_b, cudaStreamNonBlocking));
+    std::vector<cudaStream_t> a_streams, b_streams;   // a_streams[0] = stream
+    int64_t n_streams = 2;
+    void ensure_pipeline(int ring) {   // (set_option("n_streams") drops the old streams)
+        const size_t ns = size_t(std::max<int64_t>(1, std::min<int64_t>(n_streams, 8)));
+        if (a_streams.empty()) a_streams.push_back(stream);
+        while (a_streams.size() < ns) {
+            cudaStream_t x;
+            CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+            a_streams.push_back(x);
+        }
+        while (b_streams.size() < ns) {
+            cudaStream_t x;
+            CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+            b_streams.push_back(x);
+        }
         if (!ev_fork) CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
         if (!ev_join) CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
         while (int(ev_a.size()) < ring) {
@@ -470,7 +482,7 @@ struct tdg_ctx {
     DescPack pk_fwd, pk_corr, pk_misc;
     std::vector<char> host_stage;
     int64_t wave_pairs = 8;      // correlation pairs per wave (one pass-A + one pass-B launch)
-    int64_t ring = 3;            // M wave buffers in flight
+    int64_t ring = 4;            // M wave buffers in flight
     int64_t discard = 1;         // drop consumed M tiles from L2
     int64_t one_stream = 0;      // tuning: run pass B on the context stream too (no overlap)
     int64_t fwd_wave = 8;        // sequence pairs per forward-FFT wave
@@ -909,22 +921,34 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
     auto* gd = ctx->pk_corr.at<tdg::CorrGroup<G>>(og);
     auto* od = ctx->pk_corr.at<tdg::CorrPairOut>(oo);
     ctx->ensure_pipeline(ring);
+    // waves alternate over n_streams pass-A streams (the first is the context
+    // stream) and n_streams pass-B streams; more launches in flight let the
+    // latency-bound passes of neighbouring waves share the SMs
+    const int ns = int(ctx->a_streams.size());
     CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
-    CK(cudaStreamWaitEvent(ctx->stream_b, ctx->ev_fork, 0));
+    for (int i = 0; i < ns; ++i) {
+        if (i) CK(cudaStreamWaitEvent(ctx->a_streams[size_t(i)], ctx->ev_fork, 0));
+        CK(cudaStreamWaitEvent(ctx->b_streams[size_t(i)], ctx->ev_fork, 0));
+    }
     for (int wv = 0; wv < n_waves; ++wv) {
         const int r = wv % ring;
+        cudaStream_t sa = ctx->a_streams[size_t(wv % ns)];
         S.groups = gd + size_t(wv) * ngw;
         S.outs = od + size_t(wv) * wave;
-        if (wv >= ring) CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_b[size_t(r)], 0));
-        launch_pass<0>(N1, N2, ctx->stream, S);
-        CK(cudaEventRecord(ctx->ev_a[size_t(r)], ctx->stream));
-        cudaStream_t sb = ctx->one_stream ? ctx->stream : ctx->stream_b;
+        if (wv >= ring) CK(cudaStreamWaitEvent(sa, ctx->ev_b[size_t(r)], 0));
+        launch_pass<0>(N1, N2, sa, S);
+        CK(cudaEventRecord(ctx->ev_a[size_t(r)], sa));
+        cudaStream_t sb = ctx->one_stream ? sa : ctx->b_streams[size_t(wv % ns)];
         CK(cudaStreamWaitEvent(sb, ctx->ev_a[size_t(r)], 0));
         launch_pass<1>(N1, N2, sb, S);
         CK(cudaEventRecord(ctx->ev_b[size_t(r)], sb));
     }
-    CK(cudaEventRecord(ctx->ev_join, ctx->stream_b));
-    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+    for (int i = 0; i < ns; ++i)
+        for (cudaStream_t x : {ctx->a_streams[size_t(i)], ctx->b_streams[size_t(i)]})
+            if (x != ctx->stream) {
+                CK(cudaEventRecord(ctx->ev_join, x));
+                CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+            }
 }
 
 }  // namespace
@@ -962,7 +986,9 @@ void tdg_ctx_destroy(tdg_ctx* ctx) {
     for (auto e : ctx->ev_b) cudaEventDestroy(e);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
-    if (ctx->stream_b) cudaStreamDestroy(ctx->stream_b);
+    for (auto x : ctx->a_streams)
+        if (x != ctx->stream) cudaStreamDestroy(x);
+    for (auto x : ctx->b_streams) cudaStreamDestroy(x);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -1010,7 +1036,15 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
             ctx->time_kernels = value != 0;
         } else if (k == "wave_pairs")
             ctx->wave_pairs = value > 0 ? value : 8;
-        else if (k == "cta_cap_a")
+        else if (k == "n_streams") {
+            CK(cudaDeviceSynchronize());
+            for (auto x : ctx->a_streams)
+                if (x != ctx->stream) CK(cudaStreamDestroy(x));
+            for (auto x : ctx->b_streams) CK(cudaStreamDestroy(x));
+            ctx->a_streams.clear();
+            ctx->b_streams.clear();
+            ctx->n_streams = value > 0 ? value : 2;
+        } else if (k == "cta_cap_a")
             g_cta_cap[0] = int(value);
         else if (k == "cta_cap_b")
             g_cta_cap[1] = int(value);
@@ -1019,7 +1053,7 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
         else if (k == "discard")
             ctx->discard = value;
         else if (k == "ring")
-            ctx->ring = value > 0 ? value : 3;
+            ctx->ring = value > 0 ? value : 4;
 
         else if (k == "fwd_wave")
             ctx->fwd_wave = value > 0 ? value : 8;

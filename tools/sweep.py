@@ -22,7 +22,7 @@ from paper_2005_10445_b200._abi import demod_config  # noqa: E402
 def main():
     lib = capi.lib()
     cfg = demod_config()
-    bits, iq, _ = bench.make_inputs(0, 1)
+    bits, iq, _, _ = bench.make_inputs(0, 1)
     ctx = capi.Context(0)
     cs = capi.CodeSet.prepare(ctx, cfg, bench.W, bits)
     win = capi.Windows(ctx, bench.W, bench.N_WIN, len(bench.BINS))
