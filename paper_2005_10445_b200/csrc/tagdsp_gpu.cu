@@ -452,11 +452,11 @@ struct tdg_ctx {
     // streams + events of the multi-stream correlation pipeline
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::vector<cudaEvent_t> ev_a, ev_b;
-    std::vector<cudaStream_t> a_streams, b_streams;   // a_streams[0] = stream
+    std::vector<cudaStream_t> a_streams, b_streams;
+    std::vector<cudaEvent_t> ev_fwd;                  // forward-transform waves done
     int64_t n_streams = 2;
     void ensure_pipeline(int ring) {   // (set_option("n_streams") drops the old streams)
         const size_t ns = size_t(std::max<int64_t>(1, std::min<int64_t>(n_streams, 8)));
-        if (a_streams.empty()) a_streams.push_back(stream);
         while (a_streams.size() < ns) {
             cudaStream_t x;
             CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
@@ -739,7 +739,10 @@ struct FwdJob {
 
 // split = true: r1, r2 -> two Hermitian half-column spectra (window d's).
 // split = false: the packed pair's full spectrum X (code pairs), into S1.
-void run_forward(tdg_ctx* ctx, int N1, int N2, const std::vector<FwdJob>& jobs, bool split) {
+// chunk_done (optional): after each wave of `fwd_wave` jobs an event is
+// recorded on the context stream, with the number of jobs completed by then
+void run_forward(tdg_ctx* ctx, int N1, int N2, const std::vector<FwdJob>& jobs, bool split,
+                 std::vector<std::pair<size_t, cudaEvent_t>>* chunk_done = nullptr) {
     const uint64_t N = uint64_t(N1) * uint64_t(N2);
     const float2* tw1 = ctx->twiddles(N1);
     const float2* tw2 = ctx->twiddles(N2);
@@ -761,10 +764,24 @@ void run_forward(tdg_ctx* ctx, int N1, int N2, const std::vector<FwdJob>& jobs, 
             KScope ks(ctx, "fwd_pass2");
             launch_fwd2(N2, split, dim3(unsigned(N1 / 2 + 1), unsigned(n)), ctx->stream, dd + base, N1, tw2);
         }
+        if (chunk_done) {
+            const size_t k = chunk_done->size();
+            while (ctx->ev_fwd.size() <= k) {
+                cudaEvent_t e;
+                CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                ctx->ev_fwd.push_back(e);
+            }
+            CK(cudaEventRecord(ctx->ev_fwd[k], ctx->stream));
+            chunk_done->push_back({base + n, ctx->ev_fwd[k]});
+        }
     }
 }
 
-void ensure_dspec(tdg_ctx* ctx, tdg_windows* w, int N1, int N2) {
+// Window spectra of every used slot.  slot_ready (optional) receives, per
+// forward-transform wave, (slots complete, event on the context stream) so
+// that correlations of early slots can start while later slots transform.
+void ensure_dspec(tdg_ctx* ctx, tdg_windows* w, int N1, int N2,
+                  std::vector<std::pair<size_t, cudaEvent_t>>* slot_ready = nullptr) {
     const uint64_t N = uint64_t(N1) * uint64_t(N2);
     if (w->dspec_N == N) return;
     const uint64_t H = uint64_t(N1 / 2 + 1) * uint64_t(N2);
@@ -775,7 +792,9 @@ void ensure_dspec(tdg_ctx* ctx, tdg_windows* w, int N1, int N2) {
         jobs.push_back({w->d.as<float>() + s * w->W, two ? w->d.as<float>() + (s + 1) * w->W : nullptr, w->W,
                         two ? w->W : 0, w->dspec.as<float2>() + s * H, two ? w->dspec.as<float2>() + (s + 1) * H : nullptr});
     }
-    run_forward(ctx, N1, N2, jobs, true);
+    run_forward(ctx, N1, N2, jobs, true, slot_ready);
+    if (slot_ready)
+        for (auto& c : *slot_ready) c.first = std::min<size_t>(2 * c.first, w->used());   // pair jobs -> slots
     w->dspec_N = N;
 }
 
@@ -854,7 +873,9 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
     if (jobs.empty()) return;
     const int N1 = cs->N1, N2 = cs->N2;
     const uint64_t N = cs->corr_len(), H = cs->H;
-    ensure_dspec(ctx, w, N1, N2);
+    // allocate the window spectra now (their addresses go into the
+    // descriptors); the transforms themselves are enqueued after the fork
+    w->dspec.ensure(w->slots() * H * sizeof(float2));
     constexpr int G = tdg::kGroup;
     const int wave = int(std::max<int64_t>(G, ctx->wave_pairs / G * G));
     const int n_waves = int((jobs.size() + size_t(wave) - 1) / size_t(wave));
@@ -921,20 +942,33 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
     auto* gd = ctx->pk_corr.at<tdg::CorrGroup<G>>(og);
     auto* od = ctx->pk_corr.at<tdg::CorrPairOut>(oo);
     ctx->ensure_pipeline(ring);
-    // waves alternate over n_streams pass-A streams (the first is the context
-    // stream) and n_streams pass-B streams; more launches in flight let the
-    // latency-bound passes of neighbouring waves share the SMs
+    // waves alternate over n_streams pass-A and n_streams pass-B streams; more
+    // launches in flight let the latency-bound passes of neighbouring waves
+    // share the SMs.  The window spectra are transformed on the context stream
+    // after the fork, wave by wave, and a pass-A launch only waits for the
+    // transform wave that completes the slots it reads.
     const int ns = int(ctx->a_streams.size());
     CK(cudaEventRecord(ctx->ev_fork, ctx->stream));
     for (int i = 0; i < ns; ++i) {
-        if (i) CK(cudaStreamWaitEvent(ctx->a_streams[size_t(i)], ctx->ev_fork, 0));
+        CK(cudaStreamWaitEvent(ctx->a_streams[size_t(i)], ctx->ev_fork, 0));
         CK(cudaStreamWaitEvent(ctx->b_streams[size_t(i)], ctx->ev_fork, 0));
     }
+    std::vector<std::pair<size_t, cudaEvent_t>> ready;   // (slots transformed, event)
+    ensure_dspec(ctx, w, N1, N2, &ready);
+    std::vector<size_t> waited(size_t(ns), 0);            // ready[] prefix each A stream has waited for
     for (int wv = 0; wv < n_waves; ++wv) {
         const int r = wv % ring;
         cudaStream_t sa = ctx->a_streams[size_t(wv % ns)];
         S.groups = gd + size_t(wv) * ngw;
         S.outs = od + size_t(wv) * wave;
+        uint64_t top = 0;
+        for (int i = 0; i < wave && size_t(wv) * wave + i < jobs.size(); ++i)
+            top = std::max(top, jobs[size_t(wv) * wave + size_t(i)].slot + 1);
+        size_t& wt = waited[size_t(wv % ns)];
+        while (wt < ready.size() && (wt == 0 || ready[wt - 1].first < top)) {
+            CK(cudaStreamWaitEvent(sa, ready[wt].second, 0));
+            ++wt;
+        }
         if (wv >= ring) CK(cudaStreamWaitEvent(sa, ctx->ev_b[size_t(r)], 0));
         launch_pass<0>(N1, N2, sa, S);
         CK(cudaEventRecord(ctx->ev_a[size_t(r)], sa));
@@ -944,11 +978,10 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
         CK(cudaEventRecord(ctx->ev_b[size_t(r)], sb));
     }
     for (int i = 0; i < ns; ++i)
-        for (cudaStream_t x : {ctx->a_streams[size_t(i)], ctx->b_streams[size_t(i)]})
-            if (x != ctx->stream) {
-                CK(cudaEventRecord(ctx->ev_join, x));
-                CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
-            }
+        for (cudaStream_t x : {ctx->a_streams[size_t(i)], ctx->b_streams[size_t(i)]}) {
+            CK(cudaEventRecord(ctx->ev_join, x));
+            CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+        }
 }
 
 }  // namespace
@@ -986,9 +1019,9 @@ void tdg_ctx_destroy(tdg_ctx* ctx) {
     for (auto e : ctx->ev_b) cudaEventDestroy(e);
     if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
-    for (auto x : ctx->a_streams)
-        if (x != ctx->stream) cudaStreamDestroy(x);
+    for (auto x : ctx->a_streams) cudaStreamDestroy(x);
     for (auto x : ctx->b_streams) cudaStreamDestroy(x);
+    for (auto e : ctx->ev_fwd) cudaEventDestroy(e);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -1038,8 +1071,7 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
             ctx->wave_pairs = value > 0 ? value : 8;
         else if (k == "n_streams") {
             CK(cudaDeviceSynchronize());
-            for (auto x : ctx->a_streams)
-                if (x != ctx->stream) CK(cudaStreamDestroy(x));
+            for (auto x : ctx->a_streams) CK(cudaStreamDestroy(x));
             for (auto x : ctx->b_streams) CK(cudaStreamDestroy(x));
             ctx->a_streams.clear();
             ctx->b_streams.clear();
@@ -1398,8 +1430,9 @@ void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float thre
             x.bin = int32_t(s % w->n_bins);
         }
     auto* sdd = ctx->upload(ctx->pk_misc, sd);
-    ensure_dspec(ctx, w, cs->N1, cs->N2);   // forward transforms (timed as fwd_pass1/2)
     {
+        // correlation stage incl. the forward transforms it overlaps (those are
+        // also timed on their own as fwd_pass1/2)
         KScope ks(ctx, "corr");
         run_correlations(ctx, w, cs, jobs, false);
     }
