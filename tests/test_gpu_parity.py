@@ -298,8 +298,10 @@ def test_tracking_batch_parity(gpu_ctx, ref):
     iq = ref.generate_recording(cfg, seeds, 0.1, 10.0, 77, inj)
     n = iq.size // 2
     toas = [int(round(t * fs)) for _, t, _, _ in inj]
-    starts = [toas[0] - pre, toas[1] - pre, toas[2] - pre, toas[0] - pre, toas[1] - pre + 5000, 30000]
-    codes = [0, 3, 1, 2, 3, 4]    # tasks 3, 5: absent codes; task 4: shifted window
+    starts = [toas[0] - pre, toas[1] - pre, toas[2] - pre, toas[0] - pre, toas[1] - pre + 5000, 30000,
+              toas[2] - 40000]
+    codes = [0, 3, 1, 2, 3, 4, 1]  # tasks 3, 5: absent codes; task 4: shifted window; task 6: packet cut
+                                   # by the window end (partial: detector.cpp:151-153,197)
     assert all(0 <= s0 and s0 + W <= n for s0 in starts)
     cs = capi.CodeSet.prepare(gpu_ctx, cfg, W, bits)
     dets = capi.track(gpu_ctx, cfg, iq, starts, codes, cs, 0.25)
@@ -319,6 +321,7 @@ def test_tracking_batch_parity(gpu_ctx, ref):
         assert int(dets[i]["window_start"]) == s0 and int(dets[i]["code_index"]) == c
     assert dets[0]["accepted"] and dets[1]["accepted"] and dets[2]["accepted"]
     assert not dets[3]["accepted"] and not dets[5]["accepted"]
+    assert dets[6]["partial"] and not dets[6]["accepted"]
 
 
 def test_tracking_rejects_bad_tasks(gpu_ctx):
