@@ -232,8 +232,19 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Ticket& k, 
         // 32 bytes) without occupying the LSU pipe
         float2* stg = sl + role * F::STG;
         __syncwarp(0xffffffffu >> (32 - Q));   // the region's transposed inputs are consumed
+        // w_N^{k1 (c + Q e)} = tc * w_N^{k1 Q e}: exact row values every 8th e,
+        // one chained product by w_N^{k1 Q} in between
+        const float2 s1 = twr[Q + 1];
+        float2 tt = tc;
 #pragma unroll
-        for (int e = 0; e < P; ++e) stg[c + Q * e] = cmul(w[e], cmul(tc, twr[Q + e]));
+        for (int e = 0; e < P; ++e) {
+            if (e % 8 == 0) {
+                if (e) tt = cmul(tc, twr[Q + e]);
+            } else {
+                tt = cmul(tt, s1);
+            }
+            stg[c + Q * e] = cmul(w[e], tt);
+        }
     }
     if (act) {
         fence_proxy_async_smem();
