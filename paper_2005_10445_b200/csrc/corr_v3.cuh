@@ -137,24 +137,6 @@ __device__ __forceinline__ void issue_ticket(const CorrSched& S, const Ticket& k
     }
 }
 
-// Step-2 input twiddles w_L^{ac}, a = 0..P-1, for one lane c: exact table
-// values at a = 1 and every 8th a, the others by one complex multiply from
-// the previous one (at most 7 chained products: rounding stays at the
-// table's level) -- 4 table loads per column instead of P-1.
-template <int P, int Q>
-__device__ __forceinline__ void apply_step2_twiddles(float2 (&w)[P], const float2* __restrict__ tab, int c) {
-    const float2 t1 = __ldg(&tab[1 * Q + c]);
-    float2 t = t1;
-#pragma unroll
-    for (int a = 1; a < P; ++a) {
-        if (a % 8 == 0)
-            t = __ldg(&tab[a * Q + c]);
-        else if (a > 1)
-            t = cmul(t, t1);
-        w[a] = cmul(w[a], t);
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Pass A item: column pair (cp, N1-cp) x up to kGroup code pairs of one
 // window.  Code pairs are stored as the full spectrum X = FFT(dc_a + i dc_b)

@@ -289,7 +289,7 @@ void launch_fwd1(int L, dim3 grid, cudaStream_t st, const tdg::SeqPairDesc* pair
 }
 
 void launch_fwd2(int L, bool split, dim3 grid, cudaStream_t st, const tdg::SeqPairDesc* pairs, int N1,
-                 const float2* tw) {
+                 const float2* tw, const float2* twI) {
     switch (L) {
 #define X(LL, P, Q)                                                                                       \
     case LL: {                                                                                            \
@@ -297,10 +297,10 @@ void launch_fwd2(int L, bool split, dim3 grid, cudaStream_t st, const tdg::SeqPa
         const size_t sm = (size_t(2) * P * QS + 2 * LL + 2 * (P + Q)) * sizeof(float2);                   \
         if (split) {                                                                                      \
             set_smem(tdg::k_fwd_pass2<P, Q, true>, sm);                                                   \
-            tdg::k_fwd_pass2<P, Q, true><<<grid, block_for(2 * std::max(P, Q)), sm, st>>>(pairs, N1, tw);  \
+            tdg::k_fwd_pass2<P, Q, true><<<grid, block_for(2 * std::max(P, Q)), sm, st>>>(pairs, N1, tw, twI); \
         } else {                                                                                          \
             set_smem(tdg::k_fwd_pass2<P, Q, false>, sm);                                                  \
-            tdg::k_fwd_pass2<P, Q, false><<<grid, block_for(2 * std::max(P, Q)), sm, st>>>(pairs, N1, tw); \
+            tdg::k_fwd_pass2<P, Q, false><<<grid, block_for(2 * std::max(P, Q)), sm, st>>>(pairs, N1, tw, twI); \
         }                                                                                                 \
         LAUNCHED();                                                                                       \
         return;                                                                                           \
@@ -543,6 +543,32 @@ struct tdg_ctx {
     // pass-A inter-pass twiddles (csrc/corr_v3.cuh): row k1 = [w_N^{+k1 c}, c < QA]
     // [w_N^{+k1 QA e}, e < PA], computed in double with exact integer reduction
     std::map<std::pair<int, int>, std::unique_ptr<DevBuf>> twi;
+    // forward pass 2: row k1 = [w_N^{+k1 a}, a < P][w_N^{+k1 P b}, b < Q]
+    // (P x Q the pass-2 split of N2), computed in double
+    std::map<std::pair<int, int>, std::unique_ptr<DevBuf>> twf;
+    const float2* fwd_inter_twiddles(int N1, int N2) {
+        auto key = std::make_pair(N1, N2);
+        auto it = twf.find(key);
+        if (it != twf.end()) return it->second->as<float2>();
+        const PassShape& s = shape_of(N2);
+        const int st = s.P + s.Q;
+        const long long N = (long long)N1 * N2;
+        std::vector<float2> h(size_t(N1) * st);
+        const double pi = 3.14159265358979323846;
+        for (int k1 = 0; k1 < N1; ++k1)
+            for (int r = 0; r < st; ++r) {
+                const long long e = (r < s.P ? (long long)k1 * r : (long long)k1 * s.P * (r - s.P)) % N;
+                const double ang = 2.0 * pi * double(e) / double(N);
+                h[size_t(k1) * st + r] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
+            }
+        auto buf = std::make_unique<DevBuf>();
+        buf->ensure(h.size() * sizeof(float2));
+        CK(cudaMemcpy(buf->p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice));
+        const float2* p = buf->as<float2>();
+        twf[key] = std::move(buf);
+        return p;
+    }
+
     const float2* inter_twiddles(int N1, int N2) {
         auto key = std::make_pair(N1, N2);
         auto it = twi.find(key);
@@ -746,6 +772,7 @@ void run_forward(tdg_ctx* ctx, int N1, int N2, const std::vector<FwdJob>& jobs, 
     const uint64_t N = uint64_t(N1) * uint64_t(N2);
     const float2* tw1 = ctx->twiddles(N1);
     const float2* tw2 = ctx->twiddles(N2);
+    const float2* twI = ctx->fwd_inter_twiddles(N1, N2);
     const size_t wave = size_t(std::max<int64_t>(1, ctx->fwd_wave));
     ctx->T.ensure(wave * N * sizeof(float2));
     std::vector<tdg::SeqPairDesc> d(jobs.size());
@@ -762,7 +789,7 @@ void run_forward(tdg_ctx* ctx, int N1, int N2, const std::vector<FwdJob>& jobs, 
         }
         {
             KScope ks(ctx, "fwd_pass2");
-            launch_fwd2(N2, split, dim3(unsigned(N1 / 2 + 1), unsigned(n)), ctx->stream, dd + base, N1, tw2);
+            launch_fwd2(N2, split, dim3(unsigned(N1 / 2 + 1), unsigned(n)), ctx->stream, dd + base, N1, tw2, twI);
         }
         if (chunk_done) {
             const size_t k = chunk_done->size();

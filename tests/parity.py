@@ -41,9 +41,21 @@ def delta_tolerance(xc_ref, j, delta, eps, xc_scale=0.0):
     return 1e-4 + eps * max(b, xc_scale) * (1.0 + 2.0 * abs(delta)) / den
 
 
-def compare_detections(got, want, sample_rate, tie_ok=None, rel=REL, xc_ref=None, eps=2e-6):
+def pc_scale(dc, u, j):
+    """Cauchy-Schwarz scale of p_c = sum_i dc[i] u[j+i] (detector.cpp:147-165):
+    a rounding-level relative perturbation eps of dc and u (two FFT
+    implementations in the demodulation) moves p_c by at most about
+    eps * sqrt(sum dc^2 * sum u[j:j+n]^2), which for an absent code's residual
+    p_c is far above |p_c| itself."""
+    dc = np.asarray(dc, np.float64)
+    seg = np.asarray(u, np.float64)[j:j + dc.size]
+    return float(np.sqrt(np.dot(dc[:seg.size], dc[:seg.size]) * np.dot(seg, seg)))
+
+
+def compare_detections(got, want, sample_rate, tie_ok=None, rel=REL, xc_ref=None, eps=2e-6, pc_ref=None):
     """Return a list of mismatch descriptions (empty = parity).  xc_ref[code]
-    (the reference's xc rows) enables the conditioning-aware offset bound."""
+    (the reference's xc rows) enables the conditioning-aware offset bound;
+    pc_ref = (u, {code: replica_d}) the conditioning-aware p_c bound."""
     bad = []
     for g, w in zip(got, want):
         key = (int(w["code_index"]), int(w["bin"]), int(w["window_start"]))
@@ -58,6 +70,8 @@ def compare_detections(got, want, sample_rate, tie_ok=None, rel=REL, xc_ref=None
         for f in ("w_c", "peak_value", "p_c"):
             gv, wv = float(g[f]), float(w[f])
             tol = rel * abs(wv) + 1e-6 * max(abs(wv), scale, 1.0)
+            if f == "p_c" and pc_ref is not None:
+                tol += eps * pc_scale(pc_ref[1][int(w["code_index"])], pc_ref[0], int(w["peak_index"]))
             if abs(gv - wv) > tol:
                 bad.append((key, f, gv, wv))
         for f in ("q", "score"):

@@ -180,7 +180,8 @@ def test_end_to_end_desk_noisy_all_codes(gpu_ctx, ref):
         c = int(w["code_index"])
         return near_tie_margin(xc[c], int(w["peak_index"]), int(g["peak_index"])) < 1e-5
 
-    bad = compare_detections(dets, want, cfg.mod.sample_rate, tie_ok=tie_ok, xc_ref=xc, eps=1e-5)
+    bad = compare_detections(dets, want, cfg.mod.sample_rate, tie_ok=tie_ok, xc_ref=xc, eps=1e-5,
+                             pc_ref=(u, {i: s.code_replica(idx[i]) for i in range(len(bits))}))
     assert not bad, bad
 
 
@@ -214,7 +215,8 @@ def test_search_shape_parity(gpu_ctx, ref):
         c = int(w["code_index"])
         return near_tie_margin(xc[c], int(w["peak_index"]), int(g["peak_index"])) < 1e-5
 
-    bad = compare_detections(dets, want, cfg.mod.sample_rate, tie_ok=tie_ok, xc_ref=xc, eps=1e-5)
+    bad = compare_detections(dets, want, cfg.mod.sample_rate, tie_ok=tie_ok, xc_ref=xc, eps=1e-5,
+                             pc_ref=(u, {i: s.code_replica(idx[i]) for i in range(len(bits))}))
     assert not bad, bad
 
 
@@ -316,7 +318,8 @@ def test_tracking_batch_parity(gpu_ctx, ref):
         def tie_ok(g, w, xc=xc):
             return near_tie_margin(xc[0], int(w["peak_index"]), int(g["peak_index"])) < 1e-5
 
-        bad = compare_detections(dets[i:i + 1], want, fs, tie_ok=tie_ok, xc_ref={c: xc[0]}, eps=1e-5)
+        bad = compare_detections(dets[i:i + 1], want, fs, tie_ok=tie_ok, xc_ref={c: xc[0]}, eps=1e-5,
+                                 pc_ref=(u, {c: s.code_replica(idx[c])}))
         assert not bad, (i, bad)
         assert int(dets[i]["window_start"]) == s0 and int(dets[i]["code_index"]) == c
     assert dets[0]["accepted"] and dets[1]["accepted"] and dets[2]["accepted"]

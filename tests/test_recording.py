@@ -76,7 +76,8 @@ def test_detect_recording_matches_reference_and_is_deterministic(gpu_ctx, ref, t
         d, u = ref.demodulate_window(iq[2 * st:2 * (st + W)], 1000 + st, cfg)
         want = s.detect(d, u, idx, 0.25, 1000 + st, fs)
         xc = s.batch_xcorr(d, idx)
-        bad = compare_detections(recs[k * 3:(k + 1) * 3], want, fs, xc_ref=xc, eps=1e-5)
+        reps = {c: s.code_replica(idx[c]) for c in range(len(tags))}
+        bad = compare_detections(recs[k * 3:(k + 1) * 3], want, fs, xc_ref=xc, eps=1e-5, pc_ref=(u, reps))
         assert not bad, (k, bad)
     assert sum(int(r["accepted"]) for r in recs) >= 3
     text1 = recording.detections_jsonl(recs, ids, all_candidates=True)
