@@ -98,21 +98,28 @@ struct Ticket {
     int idx;
 };
 
-__device__ __forceinline__ bool ticket_noop(const CorrSched& S, const Ticket& k) {
-    if (k.type == 0) return S.groups[k.idx % S.ngw].npairs == 0;
-    return S.outs[k.idx / S.n_tiles].M == nullptr;
+// the wave's descriptors, copied to shared memory once per CTA
+struct Desc {
+    const CorrGroup<kGroup>* groups;
+    const CorrPairOut* outs;
+};
+
+__device__ __forceinline__ bool ticket_noop(const CorrSched& S, const Desc& D, const Ticket& k) {
+    if (k.type == 0) return D.groups[k.idx % S.ngw].npairs == 0;
+    return D.outs[k.idx / S.n_tiles].M == nullptr;
 }
 
 // thread 0: bulk copies of a (non-noop, ready) item into slot sl
 template <int PA, int QA, int PB, int QB>
-__device__ __forceinline__ void issue_ticket(const CorrSched& S, const Ticket& k, float2* sl, uint64_t* bar) {
+__device__ __forceinline__ void issue_ticket(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl,
+                                             uint64_t* bar) {
     using F = Fused<PA, QA, PB, QB>;
     fence_proxy_async_smem();     // earlier generic use of this slot before the async writes
     fence_proxy_async_global();   // M written by other CTAs (acquired) before the async reads
     if (k.type == 0) {
         constexpr int LA = F::LA, TWS = F::TWS;
         const int cp = k.idx / S.ngw;
-        const CorrGroup<kGroup>& gd = S.groups[k.idx % S.ngw];
+        const CorrGroup<kGroup>& gd = D.groups[k.idx % S.ngw];
         const bool self = (cp == 0) || (2 * cp == F::LB);
         const uint32_t bytes = uint32_t(LA) * 8u * uint32_t(1 + gd.npairs * (self ? 1 : 2)) + 2u * TWS * 8u;
         mbar_arrive_expect_tx(bar, bytes);
@@ -130,7 +137,7 @@ __device__ __forceinline__ void issue_ticket(const CorrSched& S, const Ticket& k
         bulk_g2s(sl + F::A_OPS + TWS, S.twI + size_t(k1b) * TWS, TWS * 8, bar);
     } else {
         constexpr int LB = F::LB;
-        const CorrPairOut& po = S.outs[k.idx / S.n_tiles];
+        const CorrPairOut& po = D.outs[k.idx / S.n_tiles];
         const int tb = k.idx % S.n_tiles;
         mbar_arrive_expect_tx(bar, LB * kTileB * 8);
         bulk_g2s_hint(sl, po.M + size_t(tb) * LB * kTileB, LB * kTileB * 8, bar, policy_evict_first());
@@ -146,14 +153,14 @@ __device__ __forceinline__ void issue_ticket(const CorrSched& S, const Ticket& k
 // i.e. one complex multiply per point; IFFT(Z) = xc_a + i xc_b.  Output: M,
 // tile-major M[(t2/kTileB)*N1*kTileB + k1*kTileB + t2%kTileB], times the
 // inter-pass twiddle w_N^{+k1 t2}.
-template <int PA, int QA, int PB, int QB>
-__device__ __forceinline__ void item_passA(const CorrSched& S, const Ticket& k, float2* sl) {
+template <int PA, int QA, int PB, int QB, class Mid>
+__device__ __forceinline__ void item_passA(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl, Mid&& mid) {
     using F = Fused<PA, QA, PB, QB>;
     constexpr int P = PA, Q = QA, L = F::LA, QS = F::QSA, TWS = F::TWS;
     constexpr int N1 = F::LB;   // pass-B length == number of columns
     const int cp = k.idx / S.ngw;
     const int tid = tid_x();
-    const CorrGroup<kGroup>& gd = S.groups[k.idx % S.ngw];
+    const CorrGroup<kGroup>& gd = D.groups[k.idx % S.ngw];
     const int npairs = gd.npairs;
     const bool self = (cp == 0) || (2 * cp == N1);
     const int role = tid >> 5;   // warp-uniform (g, col)
@@ -192,6 +199,7 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Ticket& k, 
         dft<Q, +1>(v);
     }
     __syncthreads();  // operands consumed
+    mid();            // thread 0: the next item's bulk copies
     if (act1) {
         float2* tr = sl + role * F::STG + lane * QS;
 #pragma unroll
@@ -228,14 +236,24 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Ticket& k, 
             stg[c + Q * e] = cmul(w[e], tt);
         }
     }
-    if (act) {
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-            tma_store_4d(&S.mstore, sl + role * F::STG, 0, col ? N1 - cp : cp, 0, gd.Mi[g]);
-            bulk_commit();
-        }
-    }
+    // staged column visible to the async proxy; thread 0 issues the stores
+    // after the end-of-item barrier (store_passA)
+    if (act) fence_proxy_async_smem();
+}
+
+// thread 0, after the end-of-item barrier: one TMA tensor store per active
+// (pair, column) role of the item staged in slot sl
+template <int PA, int QA, int PB, int QB>
+__device__ __forceinline__ void store_passA(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl) {
+    using F = Fused<PA, QA, PB, QB>;
+    constexpr int N1 = F::LB;
+    const int cp = k.idx / S.ngw;
+    const CorrGroup<kGroup>& gd = D.groups[k.idx % S.ngw];
+    const bool self = (cp == 0) || (2 * cp == N1);
+    for (int g = 0; g < gd.npairs; ++g)
+        for (int col = 0; col < (self ? 1 : 2); ++col)
+            tma_store_4d(&S.mstore, sl + (2 * g + col) * F::STG, 0, col ? N1 - cp : cp, 0, gd.Mi[g]);
+    bulk_commit();
 }
 
 // ---------------------------------------------------------------------------
@@ -245,10 +263,10 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Ticket& k, 
 // proj/src/detector.cpp:122-134) merged with atomicMax on packed keys, or
 // the full xc rows (batch_xcorr diagnostics).
 template <int PA, int QA, int PB, int QB>
-__device__ __forceinline__ void item_passB(const CorrSched& S, const Ticket& k, float2* sl) {
+__device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl) {
     using F = Fused<PA, QA, PB, QB>;
     constexpr int P = PB, Q = QB, ROW = F::ROWB, TB = kTileB;
-    const CorrPairOut& po = S.outs[k.idx / S.n_tiles];
+    const CorrPairOut& po = D.outs[k.idx / S.n_tiles];
     const int tb = k.idx % S.n_tiles;
     const int tid = tid_x();
     constexpr int N2 = F::LA;   // pass-A length == number of t2 columns
@@ -344,6 +362,21 @@ __global__ void __launch_bounds__(128, 3) k_corr_pass(const __grid_constant__ Co
     extern __shared__ __align__(128) unsigned char smraw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smraw);
     float2* slots = reinterpret_cast<float2*>(smraw + 128);
+    // the wave's descriptors live in shared memory (read by every item)
+    unsigned char* dsm = smraw + F::SMEM;
+    Desc D;
+    {
+        const int nb_g = TYPE == 0 ? int(S.ngw * sizeof(CorrGroup<kGroup>)) : 0;
+        const int nb_o = TYPE == 1 ? int(S.wave_pairs * sizeof(CorrPairOut)) : 0;
+        const unsigned char* src_g = reinterpret_cast<const unsigned char*>(S.groups);
+        const unsigned char* src_o = reinterpret_cast<const unsigned char*>(S.outs);
+        for (int i = threadIdx.x; i < (nb_g + nb_o) / 4; i += F::NT)
+            reinterpret_cast<uint32_t*>(dsm)[i] =
+                4 * i < nb_g ? reinterpret_cast<const uint32_t*>(src_g)[i]
+                             : reinterpret_cast<const uint32_t*>(src_o)[i - nb_g / 4];
+        D.groups = reinterpret_cast<const CorrGroup<kGroup>*>(dsm);
+        D.outs = reinterpret_cast<const CorrPairOut*>(dsm + nb_g);
+    }
     const int n_items = TYPE == 0 ? S.nA : S.nB;
     const int i0 = int(int64_t(blockIdx.x) * n_items / gridDim.x);
     const int i1 = int(int64_t(blockIdx.x + 1) * n_items / gridDim.x);
@@ -355,35 +388,46 @@ __global__ void __launch_bounds__(128, 3) k_corr_pass(const __grid_constant__ Co
     __syncthreads();
     if (threadIdx.x == 0 && i0 < i1) {
         const Ticket k0{TYPE, 0, i0};
-        if (!ticket_noop(S, k0)) issue_ticket<PA, QA, PB, QB>(S, k0, slots, &bar[0]);
+        if (!ticket_noop(S, D, k0)) issue_ticket<PA, QA, PB, QB>(S, D, k0, slots, &bar[0]);
     }
     uint32_t phases = 0u;   // bit s: parity of slot s's mbarrier
     for (int item = i0, s = 0; item < i1; ++item, s ^= 1) {
-        if (threadIdx.x == 0 && item + 1 < i1) {
-            const Ticket kn{TYPE, 0, item + 1};
-            if (!ticket_noop(S, kn)) issue_ticket<PA, QA, PB, QB>(S, kn, slots + size_t(s ^ 1) * F::SLOT, &bar[s ^ 1]);
-        }
+        // next item's bulk copies into slot s^1: pass B at the top of the item;
+        // pass A halfway through (after step 1), once the TMA stores of the
+        // item that last used slot s^1 have read their staging area
+        auto prefetch = [&]() {
+            if (threadIdx.x == 0 && item + 1 < i1) {
+                if (TYPE == 0) bulk_wait_read_all();
+                const Ticket kn{TYPE, 0, item + 1};
+                if (!ticket_noop(S, D, kn))
+                    issue_ticket<PA, QA, PB, QB>(S, D, kn, slots + size_t(s ^ 1) * F::SLOT, &bar[s ^ 1]);
+            }
+        };
+        if (TYPE == 1) prefetch();
         const Ticket k{TYPE, 0, item};
-        if (ticket_noop(S, k)) continue;
+        if (ticket_noop(S, D, k)) {
+            if (TYPE == 0) prefetch();
+            continue;
+        }
         float2* sl = slots + size_t(s) * F::SLOT;
         mbar_wait(&bar[s], (phases >> s) & 1u);
         phases ^= 1u << s;
         if (TYPE == 0) {
-            item_passA<PA, QA, PB, QB>(S, k, sl);
+            item_passA<PA, QA, PB, QB>(S, D, k, sl, prefetch);
         } else {
             // the M tile is in shared memory and its L2 lines are dead: drop
             // them without a DRAM write-back (ordered before the ring slot's
             // reuse by the kernel boundary)
-            const CorrPairOut& po = S.outs[k.idx / S.n_tiles];
+            const CorrPairOut& po = D.outs[k.idx / S.n_tiles];
             const char* tile = reinterpret_cast<const char*>(po.M + size_t(k.idx % S.n_tiles) * F::LB * kTileB);
             if (S.discard)
                 for (int l = threadIdx.x; l < F::LB * kTileB * 8 / 128; l += F::NT) discard_l2(tile + size_t(l) * 128);
-            item_passB<PA, QA, PB, QB>(S, k, sl);
+            item_passB<PA, QA, PB, QB>(S, D, k, sl);
         }
-        if (TYPE == 0 && (threadIdx.x & 31) == 0) bulk_wait_read_all();   // staged M read by the TMA engine
-        __syncthreads();   // slot s free for the prefetch of item + 2
+        __syncthreads();   // slot s consumed (pass A: its staged columns complete)
+        if (TYPE == 0 && threadIdx.x == 0) store_passA<PA, QA, PB, QB>(S, D, k, sl);
     }
-    if (TYPE == 0 && (threadIdx.x & 31) == 0) bulk_wait_all();
+    if (TYPE == 0 && threadIdx.x == 0) bulk_wait_all();
 }
 
 }  // namespace tdg

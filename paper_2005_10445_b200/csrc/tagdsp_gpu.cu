@@ -356,9 +356,12 @@ void launch_pass(int N1, int N2, cudaStream_t st, const tdg::CorrSched& S) {
     if (N1 == L1 && N2 == L2) {                                                         \
         using F = tdg::Fused<P2, Q2, P1, Q1>;                                           \
         auto* k = tdg::k_corr_pass<P2, Q2, P1, Q1, TYPE>;                               \
-        int grid = persistent_grid(k, F::NT, F::SMEM, n_items);                         \
+        /* + the wave's descriptors (copied to shared memory by every CTA) */          \
+        const size_t sm = F::SMEM + ((TYPE == 0 ? S.ngw * sizeof(tdg::CorrGroup<tdg::kGroup>)       \
+                                                : S.wave_pairs * sizeof(tdg::CorrPairOut)) + 15) / 16 * 16; \
+        int grid = persistent_grid(k, F::NT, sm, n_items);                              \
         if (g_cta_cap[TYPE] > 0) grid = std::min(grid, g_cta_cap[TYPE] * num_sms());   \
-        k<<<grid, F::NT, F::SMEM, st>>>(S);                                             \
+        k<<<grid, F::NT, sm, st>>>(S);                                                  \
         LAUNCHED();                                                                     \
         return;                                                                         \
     }
