@@ -114,8 +114,10 @@ template <int PA, int QA, int PB, int QB>
 __device__ __forceinline__ void issue_ticket(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl,
                                              uint64_t* bar) {
     using F = Fused<PA, QA, PB, QB>;
-    fence_proxy_async_smem();     // earlier generic use of this slot before the async writes
-    fence_proxy_async_global();   // M written by other CTAs (acquired) before the async reads
+    // earlier generic use of this slot before the async writes (no global
+    // proxy fence: M is written by pass A's TMA stores and read by pass B's
+    // bulk copies, both async proxy, across a kernel boundary)
+    fence_proxy_async_smem();
     if (k.type == 0) {
         constexpr int LA = F::LA, TWS = F::TWS;
         const int cp = k.idx / S.ngw;
