@@ -319,10 +319,16 @@ def main():
 
     import torch
     rank, local, world = dist_env()
+    # TDG_BENCH_BACKEND=gloo: exercise the multi-rank path with several ranks
+    # sharing fewer GPUs (collectives on host tensors) -- a test knob only;
+    # the driver's multi-GPU runs use NCCL, one rank per GPU
+    backend = os.environ.get("TDG_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
+    coll_dev = f"cuda:{local}" if backend == "nccl" else "cpu"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group(backend)
     from paper_2005_10445_b200 import capi
     from paper_2005_10445_b200._abi import DETECTION_DTYPE, demod_config
     lib = capi.lib()
@@ -367,7 +373,7 @@ def main():
             # the path's one exchange: every rank's accepted detections, all-gathered over NCCL
             from paper_2005_10445_b200 import dist as tdist
             recs = np.frombuffer(out_pin.numpy().tobytes(), dtype=DETECTION_DTYPE)
-            tdist.gather_detections(recs, code0, device=f"cuda:{local}", accepted_only=True)
+            tdist.gather_detections(recs, code0, device=coll_dev, accepted_only=True)
 
     def barrier():
         torch.cuda.synchronize()
@@ -380,7 +386,7 @@ def main():
         if world == 1:
             return x
         import torch.distributed as dist
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
