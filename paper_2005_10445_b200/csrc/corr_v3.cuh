@@ -78,9 +78,6 @@ struct CorrSched {                     // one wave
     float inv_n;
 };
 
-__device__ __forceinline__ void fence_proxy_async_global() {
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-}
 
 // threadIdx.x through a volatile read: the item bodies recompute their
 // lane-dependent addresses per item instead of letting NVVM hoist them out of
