@@ -776,7 +776,11 @@ void run_forward(tdg_ctx* ctx, int N1, int N2, const std::vector<FwdJob>& jobs, 
     const float2* tw1 = ctx->twiddles(N1);
     const float2* tw2 = ctx->twiddles(N2);
     const float2* twI = ctx->fwd_inter_twiddles(N1, N2);
-    const size_t wave = size_t(std::max<int64_t>(1, ctx->fwd_wave));
+    // at least fwd_wave pairs per launch; short transforms (tracking) fill up
+    // to kFwdScratch bytes of T so that one launch still covers the GPU
+    constexpr size_t kFwdScratch = size_t(56) << 20;
+    const size_t wave = std::min(jobs.size(), std::max(size_t(std::max<int64_t>(1, ctx->fwd_wave)),
+                                                       kFwdScratch / (N * sizeof(float2))));
     ctx->T.ensure(wave * N * sizeof(float2));
     std::vector<tdg::SeqPairDesc> d(jobs.size());
     for (size_t i = 0; i < jobs.size(); ++i) {
@@ -877,7 +881,7 @@ CUtensorMap m_store_map(float2* M, int N1, int n_tiles, uint64_t Mstride, int n_
 void launch_stats(tdg_ctx* ctx, const tdg::StatsDesc* sd, size_t n, uint32_t W, double fs, float threshold) {
     if (!n) return;
     const size_t want = size_t(num_sms()) * 8;
-    int splits = n >= want ? 1 : int(std::min<size_t>(64, (want + n - 1) / n));
+    int splits = n >= want ? 1 : int(std::min<size_t>(256, (want + n - 1) / n));
     double* partial = nullptr;
     unsigned* counters = nullptr;
     if (splits > 1) {
@@ -1182,19 +1186,27 @@ void demod_launch(tdg_ctx* ctx, const void* in, bool int16_input, uint64_t in_le
     if (W == 0 || wins.empty()) return;
     const int V = 1024 - (ctx->clen - 1);
     const uint64_t nblocks = (W + uint64_t(V) - 1) / uint64_t(V);
-    dim3 grid(unsigned((nblocks + kDemodBlk - 1) / kDemodBlk), unsigned(wins.size()));
-    const size_t sm = size_t(kDemodBlk) * (32 * 33) * sizeof(float2) + size_t(kDemodBlk) * 1024 * sizeof(float);
     const float2* tw = ctx->twiddles(1024);
     auto* wd = ctx->upload(ctx->pk_misc, wins);
     KScope ks(ctx, "demod");
+    // launches that leave the SMs mostly idle take the two-warps-per-block
+    // variant (shorter per-warp chain, one more forward transform per block)
+    const bool split = nblocks * wins.size() * 2 <= uint64_t(num_sms()) * 12;
+    auto go = [&](auto kern, int nblk, int warps_per_blk, const auto* src) {
+        dim3 grid(unsigned((nblocks + uint64_t(nblk) - 1) / uint64_t(nblk)), unsigned(wins.size()));
+        const size_t sm = size_t(nblk * warps_per_blk) * (32 * 33) * sizeof(float2) + size_t(nblk) * 1024 * sizeof(float);
+        set_smem(kern, sm);
+        kern<<<grid, nblk * warps_per_blk * 32, sm, ctx->stream>>>(src, in_len, wd, uint32_t(W), ctx->clen, n_bins,
+                                                                  slot_stride, H, eps, tw, ring_cap);
+    };
     if (int16_input) {
-        set_smem(tdg::k_demod<int32_t, kDemodBlk>, sm);
-        tdg::k_demod<int32_t, kDemodBlk><<<grid, kDemodBlk * 32, sm, ctx->stream>>>(
-            static_cast<const int32_t*>(in), in_len, wd, uint32_t(W), ctx->clen, n_bins, slot_stride, H, eps, tw, ring_cap);
+        const auto* src = static_cast<const int32_t*>(in);
+        if (split) go(tdg::k_demod<int32_t, 2, true>, 2, 2, src);
+        else go(tdg::k_demod<int32_t, kDemodBlk>, kDemodBlk, 1, src);
     } else {
-        set_smem(tdg::k_demod<float2, kDemodBlk>, sm);
-        tdg::k_demod<float2, kDemodBlk><<<grid, kDemodBlk * 32, sm, ctx->stream>>>(
-            static_cast<const float2*>(in), in_len, wd, uint32_t(W), ctx->clen, n_bins, slot_stride, H, eps, tw, 0);
+        const auto* src = static_cast<const float2*>(in);
+        if (split) go(tdg::k_demod<float2, 2, true>, 2, 2, src);
+        else go(tdg::k_demod<float2, kDemodBlk>, kDemodBlk, 1, src);
     }
     LAUNCHED();
 }

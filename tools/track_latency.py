@@ -34,14 +34,39 @@ def main():
     def call():
         capi._check(lib.tdg_track_device(ctx.handle, ctypes.byref(cfg), ctypes.c_void_p(iq_dev.data_ptr()), n, 0,
                                          capi._ptr(tasks), B, cs._h, 0.25, capi._ptr(out)))
-    for _ in range(20):
-        call()
-    ts = []
+    st = torch.cuda.ExternalStream(ctx.stream())
+
+    def measure(label):
+        for _ in range(20):
+            call()
+        ts, gs = [], []
+        for _ in range(50):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record(st)
+            call()
+            e1.record(st)
+            ts.append(time.perf_counter() - t0)
+            e1.synchronize()
+            gs.append(e0.elapsed_time(e1) * 1e3)
+        print("B=%d %-28s wall p50 %.1f us (min %.1f), stream span p50 %.1f us" %
+              (B, label, np.median(ts) * 1e6, np.min(ts) * 1e6, np.median(gs)))
+
+    measure("default")
+    for key, val in [("one_stream", 1), ("n_streams", 1)]:
+        ctx.set_option(key, val)
+        measure("%s=%d" % (key, val))
+    ctx.set_option("one_stream", 0)
+    ctx.set_option("n_streams", 2)
+    ctx.set_option("time_kernels", 1)
+    ctx.kernel_time_reset()
     for _ in range(50):
-        t0 = time.perf_counter()
         call()
-        ts.append(time.perf_counter() - t0)
-    print("B=%d wall p50 %.1f us, min %.1f us" % (B, np.median(ts) * 1e6, np.min(ts) * 1e6))
+    for k in ["demod", "fwd_pass1", "fwd_pass2", "stats"]:
+        n_, ms = ctx.kernel_time(k)
+        if n_:
+            print("  %-10s %.1f us/call" % (k, ms / 50 * 1e3))
+    ctx.set_option("time_kernels", 0)
     torch.cuda.cudart().cudaProfilerStart()
     call()
     torch.cuda.cudart().cudaProfilerStop()
