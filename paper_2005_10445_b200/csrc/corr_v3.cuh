@@ -83,6 +83,12 @@ struct CorrSched {                     // one wave
 // lane-dependent addresses per item instead of letting NVVM hoist them out of
 // the persistent loop, where pass A's and pass B's invariants together would
 // stay live across both bodies and spill.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ int tid_x() {
     int t;
     asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
@@ -269,6 +275,12 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
     const int tb = k.idx % S.n_tiles;
     const int tid = tid_x();
     constexpr int N2 = F::LA;   // pass-A length == number of t2 columns
+    // the pair's best magnitudes so far (high words of the packed keys)
+    float cur_a = 0.f, cur_b = 0.f;
+    if (!S.write_xc) {
+        cur_a = __uint_as_float(uint32_t(ld_relaxed_u64(po.key_a) >> 32));
+        if (po.key_b) cur_b = __uint_as_float(uint32_t(ld_relaxed_u64(po.key_b) >> 32));
+    }
     const uint32_t W = S.W;
     // step 1: task (a, t2l), t2l fastest
     const int t2l1 = tid % TB, a1 = tid / TB;
@@ -289,15 +301,14 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
     const int t2l = tid % TB, c = tid / TB;
     const int t2 = tb * TB + t2l;
     float best_a = -1.f, best_b = -1.f;
-    uint32_t idx_a = 0, idx_b = 0;
+    int e_lim = 0;
+    float2 w[P];
     if (c < Q) {
-        float2 w[P];
 #pragma unroll
         for (int a = 0; a < P; ++a) w[a] = sl[a * ROW + c * TB + t2l];
         apply_step2_twiddles<P, Q>(w, S.twB, c);
         dft<P, +1>(w);
         // valid lags t = t2 + N2*(c + Q*e) < W form a prefix e < e_lim
-        int e_lim = 0;
         if (t2 < N2 && uint32_t(t2) < W) {
             const int t1max = int((W - 1u - uint32_t(t2)) / uint32_t(N2));
             e_lim = t1max >= c ? (t1max - c) / Q + 1 : 0;
@@ -312,41 +323,61 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
                     if (po.xc_b) po.xc_b[t] = w[e].y * S.inv_n;
                 }
             }
-        } else if (e_lim > 0) {
-            // t increases with e: strict '>' keeps the first index
-            int ea = 0, eb = 0;
+        } else if (e_lim == P) {
+#pragma unroll
+            for (int e = 0; e < P; ++e) {
+                best_a = fmaxf(best_a, fabsf(w[e].x));
+                best_b = fmaxf(best_b, fabsf(w[e].y));
+            }
+        } else {
 #pragma unroll
             for (int e = 0; e < P; ++e) {
                 if (e < e_lim) {
-                    const float ma = fabsf(w[e].x), mb = fabsf(w[e].y);
-                    if (ma > best_a) {
-                        best_a = ma;
-                        ea = e;
-                    }
-                    if (mb > best_b) {
-                        best_b = mb;
-                        eb = e;
-                    }
+                    best_a = fmaxf(best_a, fabsf(w[e].x));
+                    best_b = fmaxf(best_b, fabsf(w[e].y));
                 }
             }
-            idx_a = uint32_t(t2) + uint32_t(N2) * uint32_t(c + Q * ea);
-            idx_b = uint32_t(t2) + uint32_t(N2) * uint32_t(c + Q * eb);
         }
     }
     if (!S.write_xc) {
-        // packed keys order by magnitude, then smallest index: exact first-index ties
-        unsigned long long ka = best_a >= 0.f ? peak_key(best_a, idx_a) : 0ull;
-        unsigned long long kb = best_b >= 0.f ? peak_key(best_b, idx_b) : 0ull;
+        // first-index argmax.  Warp maxima of |Re|, |Im| first; only warps
+        // whose maximum can still win against the pair's best so far (read at
+        // item start -- an older value only makes more warps search) locate
+        // their first index and merge packed keys (magnitude, then smallest
+        // index: exact first-index ties) with atomicMax.
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long xa = __shfl_xor_sync(0xffffffffu, ka, o);
-            const unsigned long long xb = __shfl_xor_sync(0xffffffffu, kb, o);
-            ka = xa > ka ? xa : ka;
-            kb = xb > kb ? xb : kb;
+            best_a = fmaxf(best_a, __shfl_xor_sync(0xffffffffu, best_a, o));
+            best_b = fmaxf(best_b, __shfl_xor_sync(0xffffffffu, best_b, o));
         }
-        if ((tid & 31) == 0) {
-            if (ka) atomicMax(po.key_a, ka);
-            if (kb && po.key_b) atomicMax(po.key_b, kb);
+        const bool need_a = best_a >= 0.f && best_a >= cur_a;
+        const bool need_b = best_b >= 0.f && po.key_b && best_b >= cur_b;
+        if (need_a || need_b) {   // warp-uniform
+            int ea = P, eb = P;
+            if (c < Q) {
+#pragma unroll
+                for (int e = P - 1; e >= 0; --e) {
+                    if (e < e_lim) {
+                        if (fabsf(w[e].x) == best_a) ea = e;
+                        if (fabsf(w[e].y) == best_b) eb = e;
+                    }
+                }
+            }
+            unsigned long long ka = need_a && ea < P
+                ? peak_key(best_a, uint32_t(t2) + uint32_t(N2) * uint32_t(c + Q * ea)) : 0ull;
+            unsigned long long kb = need_b && eb < P
+                ? peak_key(best_b, uint32_t(t2) + uint32_t(N2) * uint32_t(c + Q * eb)) : 0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long xa = __shfl_xor_sync(0xffffffffu, ka, o);
+                const unsigned long long xb = __shfl_xor_sync(0xffffffffu, kb, o);
+                ka = xa > ka ? xa : ka;
+                kb = xb > kb ? xb : kb;
+            }
+            if ((tid & 31) == 0) {
+                if (ka) atomicMax(po.key_a, ka);
+                if (kb) atomicMax(po.key_b, kb);
+            }
         }
     }
 }
