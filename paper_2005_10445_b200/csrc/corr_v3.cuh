@@ -79,16 +79,16 @@ struct CorrSched {                     // one wave
 };
 
 
-// threadIdx.x through a volatile read: the item bodies recompute their
-// lane-dependent addresses per item instead of letting NVVM hoist them out of
-// the persistent loop, where pass A's and pass B's invariants together would
-// stay live across both bodies and spill.
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
     unsigned long long v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
 
+// threadIdx.x through a volatile read: the item bodies recompute their
+// lane-dependent addresses per item instead of letting NVVM hoist them out of
+// the persistent loop, where pass A's and pass B's invariants together would
+// stay live across both bodies and spill.
 __device__ __forceinline__ int tid_x() {
     int t;
     asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
