@@ -447,7 +447,7 @@ struct tdg_ctx {
     cudaStream_t stream = nullptr;
     std::map<int, std::unique_ptr<DevBuf>> tw;   // per pass length: w_L^{+a c}, index a*Q + c
     // filter spectra cache
-    std::string hkey;
+    std::vector<double> hkey;   // filter_spectra cache key
     DevBuf hspec;
     int clen = 0;
     // scratch
@@ -482,7 +482,7 @@ struct tdg_ctx {
     }
     tdg_windows* search_win = nullptr;   // cached window set of tdg_search (reused across calls)
     tdg_windows* track_win = nullptr;    // cached window set of tdg_track (capacity grows)
-    DescPack pk_fwd, pk_corr, pk_misc;
+    DescPack pk_fwd, pk_corr, pk_misc, pk_stats;   // one per stage: no stage waits on another's staging copy
     std::vector<char> host_stage;
     int64_t wave_pairs = 8;      // correlation pairs per wave (one pass-A + one pass-B launch)
     int64_t ring = 4;            // M wave buffers in flight
@@ -607,15 +607,11 @@ struct tdg_ctx {
     // FFT_1024 spectra of the LO-shifted composed filters for a bin set.
     const float2* filter_spectra(const tdg_demod_config& c, const std::vector<double>& bins) {
         validate_cfg(c);
-        char key[256];
-        snprintf(key, sizeof(key), "%.17g/%.17g/%.17g/%.17g/%llu/%.17g/%.17g/%llu|", c.mod.sample_rate, c.mod.bit_rate,
-                 c.mod.freq_one, c.mod.freq_zero, (unsigned long long)c.mod.packet_bits, c.bandpass_center,
-                 c.bandpass_width, (unsigned long long)c.bandpass_taps);
-        std::string k(key);
-        for (double b : bins) {
-            snprintf(key, sizeof(key), "%.17g,", b);
-            k += key;
-        }
+        // cache key: the parameters the composed filters depend on, then the bins
+        std::vector<double> k{c.mod.sample_rate,     c.mod.bit_rate,   c.mod.freq_one,
+                              c.mod.freq_zero,       double(c.mod.packet_bits),
+                              c.bandpass_center,     c.bandpass_width, double(c.bandpass_taps)};
+        k.insert(k.end(), bins.begin(), bins.end());
         if (k == hkey) return hspec.as<float2>();
         const size_t spb = samples_per_bit(c.mod);
         std::vector<cfloat> hbp, hm;
@@ -975,6 +971,17 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
     S.inv_n = 1.0f / float(N);
     auto* gd = ctx->pk_corr.at<tdg::CorrGroup<G>>(og);
     auto* od = ctx->pk_corr.at<tdg::CorrPairOut>(oo);
+    if (n_waves == 1) {
+        // one wave (small tracking batches): nothing to overlap, so no fork,
+        // events or join -- the transforms and both passes in order on the
+        // context stream (API calls are most of a small batch's latency)
+        ensure_dspec(ctx, w, N1, N2);
+        S.groups = gd;
+        S.outs = od;
+        launch_pass<0>(N1, N2, ctx->stream, S);
+        launch_pass<1>(N1, N2, ctx->stream, S);
+        return;
+    }
     ctx->ensure_pipeline(ring);
     // waves alternate over n_streams pass-A and n_streams pass-B streams; more
     // launches in flight let the latency-bound passes of neighbouring waves
@@ -1139,13 +1146,13 @@ void finish_codeset(tdg_ctx* ctx, tdg_codeset* cs, const float* d, const float* 
     cs->abs_dev.ensure(n * sizeof(float));
     cs->rep_cap = 0;
     for (uint64_t l : lens) cs->rep_cap = std::max(cs->rep_cap, l);
-    cs->rep_cap = std::max<uint64_t>(cs->rep_cap, 1);
+    cs->rep_cap = (std::max<uint64_t>(cs->rep_cap, 1) + 3) & ~uint64_t(3);   // 16-byte rows (stats vector loads)
     cs->rep.ensure(n * cs->rep_cap * sizeof(float));
     std::vector<tdg::SupportDesc> sd(n);
     for (uint64_t i = 0; i < n; ++i)
         sd[i] = {d + i * stride, u ? u + i * stride : nullptr, lens[i], cs->rep.as<float>() + i * cs->rep_cap,
                  cs->rep_cap, cs->nlen_dev.as<uint64_t>() + i, cs->energy_dev.as<float>() + i, cs->abs_dev.as<float>() + i};
-    auto* sdd = ctx->upload(ctx->pk_misc, sd);
+    auto* sdd = ctx->upload(ctx->pk_stats, sd);
     tdg::k_support<<<unsigned(n), 1024, 0, ctx->stream>>>(sdd);
     LAUNCHED();
     cs->nlen.resize(n);
@@ -1471,7 +1478,7 @@ void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float thre
             x.code_index = int32_t(c);
             x.bin = int32_t(s % w->n_bins);
         }
-    auto* sdd = ctx->upload(ctx->pk_misc, sd);
+    auto* sdd = ctx->upload(ctx->pk_stats, sd);
     {
         // correlation stage incl. the forward transforms it overlaps (those are
         // also timed on their own as fwd_pass1/2)
@@ -1627,7 +1634,7 @@ void track_impl(tdg_ctx* ctx, const tdg_demod_config* cfg, const SampleSource& s
         x.code_index = int32_t(c);
         x.bin = 0;
     }
-    auto* sdd = ctx->upload(ctx->pk_misc, sd);
+    auto* sdd = ctx->upload(ctx->pk_stats, sd);
     launch_stats(ctx, sdd, n_tasks, uint32_t(W), cfg->mod.sample_rate, threshold);
     if (out) {
         CK(cudaMemcpyAsync(out, ctx->det_dev.p, n_tasks * sizeof(tdg_detection), cudaMemcpyDeviceToHost,
