@@ -185,6 +185,51 @@ def test_end_to_end_desk_noisy_all_codes(gpu_ctx, ref):
     assert not bad, bad
 
 
+def test_detect_statistics_alignment_paths(gpu_ctx, ref):
+    """detect() back half (statistics, parabola, score) on odd window lengths
+    and several slots, so the statistics kernel sees every 16-byte phase of
+    d[j-1] and u[j] (vector path), misaligned slots (scalar path), peaks near
+    the window end (partial, edge lags) and peak index 0."""
+    from paper_2005_10445_b200 import capi
+    rng = np.random.default_rng(77)
+    for W in (4099, 4096 + 1024):
+        dcs = [ref.gaussian(9100 + i, n) for i, n in enumerate((100, 257, 1000, 1501, 2100))]
+        cs = _cs_from(capi, gpu_ctx, dcs, W, ref)
+        s = ref.Session()
+        N = ref.pad_length(W + max(x.size for x in dcs))
+        idx = [s.make_transformed(x, x, W, N) for x in dcs]
+        n_slots = 4
+        win = capi.Windows(gpu_ctx, W, n_slots)
+        want, xcs, us = [], [], []
+        for slot in range(n_slots):
+            d = (0.05 * rng.standard_normal(W)).astype(np.float32)
+            # code k at offset placed per slot: start of window, interior, and
+            # across the end (partial statistics)
+            for k, dc in enumerate(dcs):
+                off = [0, 1 + 37 * slot + k, 1777 + 3 * slot + k, W - 60 - k][(slot + k) % 4]
+                m = min(dc.size, W - off)
+                d[off:off + m] += dc[:m]
+            u = (0.5 * d + 0.01 * rng.standard_normal(W)).astype(np.float32)
+            win.set_du(slot, d, u, 1000 * slot)
+            want.extend(s.detect(d, u, idx, 0.25, 1000 * slot, 8.0e6))
+            xcs.append(s.batch_xcorr(d, idx))
+            us.append(u)
+        got = capi.detect(gpu_ctx, win, cs, 0.25, 8.0e6)
+        nc = len(dcs)
+        for slot in range(n_slots):
+            g = got[slot * nc:(slot + 1) * nc]
+            w = want[slot * nc:(slot + 1) * nc]
+            xc = xcs[slot]
+
+            def tie_ok(a, b):
+                c = int(b["code_index"])
+                return near_tie_margin(xc[c], int(b["peak_index"]), int(a["peak_index"])) < 1e-5
+
+            bad = compare_detections(g, w, 8.0e6, tie_ok=tie_ok, xc_ref=xc,
+                                     pc_ref=(us[slot], {i: dcs[i] for i in range(nc)}))
+            assert not bad, (W, slot, bad)
+
+
 @pytest.mark.slow
 def test_search_shape_parity(gpu_ctx, ref):
     """Default 8 Ms/s search shape (W = 800,000, N = 870,912): one injected
