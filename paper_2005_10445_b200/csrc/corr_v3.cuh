@@ -394,6 +394,21 @@ __global__ void __launch_bounds__(128, 3) k_corr_pass(const __grid_constant__ Co
     float2* slots = reinterpret_cast<float2*>(smraw + 128);
     // the wave's descriptors live in shared memory (read by every item)
     unsigned char* dsm = smraw + F::SMEM;
+    const int n_items = TYPE == 0 ? S.nA : S.nB;
+    const int i0 = int(int64_t(blockIdx.x) * n_items / gridDim.x);
+    const int i1 = int(int64_t(blockIdx.x + 1) * n_items / gridDim.x);
+    // thread 0 starts the first item's bulk copies from the global descriptors
+    // while the CTA stages the descriptors in shared memory
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_fence_init();
+        if (i0 < i1) {
+            const Desc Dg{S.groups, S.outs};
+            const Ticket k0{TYPE, 0, i0};
+            if (!ticket_noop(S, Dg, k0)) issue_ticket<PA, QA, PB, QB>(S, Dg, k0, slots, &bar[0]);
+        }
+    }
     Desc D;
     {
         const int nb_g = TYPE == 0 ? int(S.ngw * sizeof(CorrGroup<kGroup>)) : 0;
@@ -407,19 +422,7 @@ __global__ void __launch_bounds__(128, 3) k_corr_pass(const __grid_constant__ Co
         D.groups = reinterpret_cast<const CorrGroup<kGroup>*>(dsm);
         D.outs = reinterpret_cast<const CorrPairOut*>(dsm + nb_g);
     }
-    const int n_items = TYPE == 0 ? S.nA : S.nB;
-    const int i0 = int(int64_t(blockIdx.x) * n_items / gridDim.x);
-    const int i1 = int(int64_t(blockIdx.x + 1) * n_items / gridDim.x);
-    if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        mbar_fence_init();
-    }
     __syncthreads();
-    if (threadIdx.x == 0 && i0 < i1) {
-        const Ticket k0{TYPE, 0, i0};
-        if (!ticket_noop(S, D, k0)) issue_ticket<PA, QA, PB, QB>(S, D, k0, slots, &bar[0]);
-    }
     uint32_t phases = 0u;   // bit s: parity of slot s's mbarrier
     for (int item = i0, s = 0; item < i1; ++item, s ^= 1) {
         // next item's bulk copies into slot s^1: pass B at the top of the item;
