@@ -350,8 +350,11 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
             best_a = fmaxf(best_a, __shfl_xor_sync(0xffffffffu, best_a, o));
             best_b = fmaxf(best_b, __shfl_xor_sync(0xffffffffu, best_b, o));
         }
-        const bool need_a = best_a >= 0.f && best_a >= cur_a;
-        const bool need_b = best_b >= 0.f && po.key_b && best_b >= cur_b;
+        // each lane read the pair's best on its own, so another CTA's atomicMax
+        // can land between lanes: vote, so the branch below (full-warp
+        // shuffles) is taken by every lane or none
+        const bool need_a = __any_sync(0xffffffffu, best_a >= 0.f && best_a >= cur_a);
+        const bool need_b = __any_sync(0xffffffffu, best_b >= 0.f && po.key_b != nullptr && best_b >= cur_b);
         if (need_a || need_b) {   // warp-uniform
             int ea = P, eb = P;
             if (c < Q) {

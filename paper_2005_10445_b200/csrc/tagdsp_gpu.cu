@@ -28,6 +28,17 @@ namespace {
 
 thread_local std::string g_err;
 std::atomic<uint64_t> g_launches{0};
+// bumped by every device allocation and free: a captured CUDA graph is only
+// replayed while no buffer it may reference has moved
+std::atomic<uint64_t> g_dev_epoch{0};
+// small tracking batches as CUDA graphs (track_graph): 0 = stream ops issued
+// normally, 1 = being captured, 2 = replay -- host-side descriptor rebuild
+// only, every stream op is skipped (the instantiated graph carries them)
+thread_local int tl_graph_mode = 0;
+#define STREAM_OPS (tl_graph_mode != 2)
+// a replayed tracking graph: its kernels were counted as launched while the
+// host pass walked the launch sites
+#define LAUNCHED_GRAPH() ck(cudaGetLastError(), "graph launch")
 
 struct Error : std::runtime_error {
     int code;
@@ -48,10 +59,12 @@ void ck(cudaError_t e, const char* what) {
 }
 
 #define CK(x) ck((x), #x)
-#define LAUNCHED()                                              \
-    do {                                                        \
-        g_launches.fetch_add(1, std::memory_order_relaxed);     \
-        ck(cudaGetLastError(), "kernel launch");                \
+#define TDG_STR2(x) #x
+#define TDG_STR(x) TDG_STR2(x)
+#define LAUNCHED()                                                                  \
+    do {                                                                            \
+        if (tl_graph_mode != 1) g_launches.fetch_add(1, std::memory_order_relaxed); \
+        ck(cudaGetLastError(), "kernel launch (" TDG_STR(__LINE__) ")");            \
     } while (0)
 
 template <class F>
@@ -81,7 +94,10 @@ struct DevBuf {
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            cudaFree(p);
+            g_dev_epoch.fetch_add(1, std::memory_order_relaxed);
+        }
         p = nullptr;
         bytes = 0;
     }
@@ -89,6 +105,7 @@ struct DevBuf {
         if (b <= bytes) return;
         release();
         CK(cudaMalloc(&p, b));
+        g_dev_epoch.fetch_add(1, std::memory_order_relaxed);
         bytes = b;
     }
     template <class T>
@@ -123,6 +140,7 @@ struct DescPack {
             size_t ncap = std::max(need, cap * 2 + 4096);
             char* nh = nullptr;
             CK(cudaHostAlloc(reinterpret_cast<void**>(&nh), ncap, cudaHostAllocDefault));
+            g_dev_epoch.fetch_add(1, std::memory_order_relaxed);   // staging moved
             if (host) {
                 std::memcpy(nh, host, used);
                 cudaFreeHost(host);
@@ -135,9 +153,10 @@ struct DescPack {
         return off;
     }
     void commit(cudaStream_t st) {
-        if (!done) CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
         dev.ensure(std::max<size_t>(used, 256));
-        if (used) CK(cudaMemcpyAsync(dev.p, host, used, cudaMemcpyHostToDevice, st));
+        if (used && STREAM_OPS) CK(cudaMemcpyAsync(dev.p, host, used, cudaMemcpyHostToDevice, st));
+        if (tl_graph_mode) return;   // graph packs: the caller orders reuse (synchronous calls)
+        if (!done) CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
         CK(cudaEventRecord(done, st));
         pending = true;
     }
@@ -253,18 +272,20 @@ bool choose_corr_len(uint64_t need, int* n1, int* n2) {
 // Kernel dispatch by pass length
 template <class T>
 void set_smem(T* kernel, size_t bytes) {
-    // once per (kernel, size): the attribute call costs a few microseconds,
-    // which matters for latency-bound tracking batches
+    // the opt-in limit only ever rises per (kernel, device): a launch with
+    // fewer bytes than an earlier one must not lower it under that one.  The
+    // attribute call costs a few microseconds (latency-bound tracking
+    // batches), so it is made only when the limit has to rise.
     static std::mutex mu;
-    static std::map<std::tuple<const void*, size_t, int>, bool> done;
+    static std::map<std::pair<const void*, int>, size_t> limit;
     if (bytes <= 48 * 1024) return;
     int dev = 0;
     CK(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_tuple(reinterpret_cast<const void*>(kernel), bytes, dev);
-    if (done.count(key)) return;
+    size_t& cur = limit[std::make_pair(reinterpret_cast<const void*>(kernel), dev)];
+    if (bytes <= cur) return;
     CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
-    done[key] = true;
+    cur = bytes;
 }
 
 int block_for(int tasks) {
@@ -278,7 +299,7 @@ void launch_fwd1(int L, dim3 grid, cudaStream_t st, const tdg::SeqPairDesc* pair
     case LL: {                                                                             \
         const size_t sm = size_t(P) * Q * kTB * sizeof(float2);                            \
         set_smem(tdg::k_fwd_pass1<P, Q, kTB>, sm);                                         \
-        tdg::k_fwd_pass1<P, Q, kTB><<<grid, block_for(std::max(P, Q) * kTB), sm, st>>>(pairs, N2, tw); \
+        if (STREAM_OPS) tdg::k_fwd_pass1<P, Q, kTB><<<grid, block_for(std::max(P, Q) * kTB), sm, st>>>(pairs, N2, tw); \
         LAUNCHED();                                                                        \
         return;                                                                            \
     }
@@ -297,10 +318,10 @@ void launch_fwd2(int L, bool split, dim3 grid, cudaStream_t st, const tdg::SeqPa
         const size_t sm = (size_t(2) * P * QS + 2 * LL + 2 * (P + Q)) * sizeof(float2);                   \
         if (split) {                                                                                      \
             set_smem(tdg::k_fwd_pass2<P, Q, true>, sm);                                                   \
-            tdg::k_fwd_pass2<P, Q, true><<<grid, block_for(2 * std::max(P, Q)), sm, st>>>(pairs, N1, tw, twI); \
+            if (STREAM_OPS) tdg::k_fwd_pass2<P, Q, true><<<grid, block_for(2 * std::max(P, Q)), sm, st>>>(pairs, N1, tw, twI); \
         } else {                                                                                          \
             set_smem(tdg::k_fwd_pass2<P, Q, false>, sm);                                                  \
-            tdg::k_fwd_pass2<P, Q, false><<<grid, block_for(2 * std::max(P, Q)), sm, st>>>(pairs, N1, tw, twI); \
+            if (STREAM_OPS) tdg::k_fwd_pass2<P, Q, false><<<grid, block_for(2 * std::max(P, Q)), sm, st>>>(pairs, N1, tw, twI); \
         }                                                                                                 \
         LAUNCHED();                                                                                       \
         return;                                                                                           \
@@ -337,8 +358,8 @@ int persistent_grid(K* kernel, int threads, size_t smem, int n_items) {
         if (it != cache.end()) {
             per_sm = it->second;
         } else {
-            CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
             CK(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            set_smem(kernel, smem);
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
             cache[key] = per_sm;
         }
@@ -361,7 +382,7 @@ void launch_pass(int N1, int N2, cudaStream_t st, const tdg::CorrSched& S) {
                                                 : S.wave_pairs * sizeof(tdg::CorrPairOut)) + 15) / 16 * 16; \
         int grid = persistent_grid(k, F::NT, sm, n_items);                              \
         if (g_cta_cap[TYPE] > 0) grid = std::min(grid, g_cta_cap[TYPE] * num_sms());   \
-        k<<<grid, F::NT, sm, st>>>(S);                                                  \
+        if (STREAM_OPS) k<<<grid, F::NT, sm, st>>>(S);                                  \
         LAUNCHED();                                                                     \
         return;                                                                         \
     }
@@ -442,6 +463,34 @@ struct KScope {   // records a CUDA event pair around one launch when timing is 
     ~KScope();
 };
 
+struct DescPacks {
+    DescPack fwd, corr, misc, stats;
+};
+
+// A small tracking batch (one correlation wave) captured as a CUDA graph:
+// demod, forward transforms, both correlation passes and the statistics with
+// their descriptor uploads from this entry's own pinned staging.  A replay
+// rewrites the staging in place (same offsets) and launches the graph; it is
+// valid while nothing it references has moved (g_dev_epoch) and the key --
+// batch size, code set, window, input block and every kernel parameter that
+// comes from the configuration -- matches.
+struct TrackGraph {
+    std::vector<double> key;
+    const void* cs = nullptr;
+    const void* base = nullptr;
+    uint64_t epoch = 0;
+    int state = 0;   // 1: seen once (every cache warm), 2: captured
+    cudaGraphExec_t exec = nullptr;
+    DescPacks packs;
+    uint64_t last_use = 0;
+    TrackGraph() = default;
+    TrackGraph(const TrackGraph&) = delete;
+    TrackGraph& operator=(const TrackGraph&) = delete;
+    ~TrackGraph() {
+        if (exec) cudaGraphExecDestroy(exec);
+    }
+};
+
 struct tdg_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -482,7 +531,13 @@ struct tdg_ctx {
     }
     tdg_windows* search_win = nullptr;   // cached window set of tdg_search (reused across calls)
     tdg_windows* track_win = nullptr;    // cached window set of tdg_track (capacity grows)
-    DescPack pk_fwd, pk_corr, pk_misc, pk_stats;   // one per stage: no stage waits on another's staging copy
+    // descriptor staging, one pack per stage (no stage waits on another's
+    // staging copy); a captured tracking graph brings its own set
+    DescPacks own_packs;
+    DescPacks* pk = &own_packs;
+    std::vector<std::unique_ptr<TrackGraph>> track_graphs;
+    int64_t track_graphs_on = 1;   // small tracking batches replayed as CUDA graphs
+    uint64_t graph_clock = 0;
     std::vector<char> host_stage;
     int64_t wave_pairs = 8;      // correlation pairs per wave (one pass-A + one pass-B launch)
     int64_t ring = 4;            // M wave buffers in flight
@@ -648,7 +703,7 @@ struct tdg_ctx {
 };
 
 KScope::KScope(tdg_ctx* c, const char* n) : ctx(c), name(n) {
-    if (ctx->time_kernels) {
+    if (ctx->time_kernels && !tl_graph_mode) {
         a = ctx->ev();
         cudaEventRecord(a, ctx->stream);
     }
@@ -783,7 +838,7 @@ void run_forward(tdg_ctx* ctx, int N1, int N2, const std::vector<FwdJob>& jobs, 
         const auto& j = jobs[i];
         d[i] = {j.r1, j.r2, j.len1, j.len2, ctx->T.as<float2>() + (i % wave) * N, j.S1, j.S2};
     }
-    tdg::SeqPairDesc* dd = ctx->upload(ctx->pk_fwd, d);
+    tdg::SeqPairDesc* dd = ctx->upload(ctx->pk->fwd, d);
     for (size_t base = 0; base < jobs.size(); base += wave) {
         const size_t n = std::min(wave, jobs.size() - base);
         {
@@ -884,17 +939,19 @@ void launch_stats(tdg_ctx* ctx, const tdg::StatsDesc* sd, size_t n, uint32_t W, 
         ctx->stats_part.ensure(n * size_t(splits) * 5 * sizeof(double));
         if (ctx->stats_ctr.bytes < n * sizeof(unsigned)) {
             ctx->stats_ctr.ensure(n * sizeof(unsigned));
-            CK(cudaMemsetAsync(ctx->stats_ctr.p, 0, ctx->stats_ctr.bytes, ctx->stream));
+            if (STREAM_OPS) CK(cudaMemsetAsync(ctx->stats_ctr.p, 0, ctx->stats_ctr.bytes, ctx->stream));
         }
         partial = ctx->stats_part.as<double>();
         counters = ctx->stats_ctr.as<unsigned>();
     }
     KScope ks(ctx, "stats");
-    if (splits > 1)
-        tdg::k_stats<true><<<unsigned(n * size_t(splits)), 256, 0, ctx->stream>>>(sd, W, fs, threshold, splits,
-                                                                             partial, counters);
-    else
-        tdg::k_stats<false><<<unsigned(n), 256, 0, ctx->stream>>>(sd, W, fs, threshold, 1, nullptr, nullptr);
+    if (STREAM_OPS) {
+        if (splits > 1)
+            tdg::k_stats<true><<<unsigned(n * size_t(splits)), 256, 0, ctx->stream>>>(sd, W, fs, threshold, splits,
+                                                                                 partial, counters);
+        else
+            tdg::k_stats<false><<<unsigned(n), 256, 0, ctx->stream>>>(sd, W, fs, threshold, 1, nullptr, nullptr);
+    }
     LAUNCHED();
 }
 
@@ -949,10 +1006,10 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
             o.xc_b = jb.xc_b;
         }
     }
-    ctx->pk_corr.begin();
-    const size_t og = ctx->pk_corr.add(groups);
-    const size_t oo = ctx->pk_corr.add(outs);
-    ctx->pk_corr.commit(ctx->stream);
+    ctx->pk->corr.begin();
+    const size_t og = ctx->pk->corr.add(groups);
+    const size_t oo = ctx->pk->corr.add(outs);
+    ctx->pk->corr.commit(ctx->stream);
     tdg::CorrSched S{};
     S.mstore = m_store_map(ctx->M.as<float2>(), N1, n_tiles, Mstride, ring * wave);
     S.twA = ctx->twiddles(N2);
@@ -969,8 +1026,8 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
     S.discard = ctx->discard ? 1 : 0;
     S.W = uint32_t(w->W);
     S.inv_n = 1.0f / float(N);
-    auto* gd = ctx->pk_corr.at<tdg::CorrGroup<G>>(og);
-    auto* od = ctx->pk_corr.at<tdg::CorrPairOut>(oo);
+    auto* gd = ctx->pk->corr.at<tdg::CorrGroup<G>>(og);
+    auto* od = ctx->pk->corr.at<tdg::CorrPairOut>(oo);
     if (n_waves == 1) {
         // one wave (small tracking batches): nothing to overlap, so no fork,
         // events or join -- the transforms and both passes in order on the
@@ -1105,6 +1162,7 @@ int tdg_kernel_time_reset(tdg_ctx* ctx) {
 int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
     return guard([&] {
         std::string k(key);
+        ctx->track_graphs.clear();   // captured launch configurations may change
         if (k == "time_kernels") {
             ctx->collect();
             ctx->time_kernels = value != 0;
@@ -1127,7 +1185,8 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
             ctx->discard = value;
         else if (k == "ring")
             ctx->ring = value > 0 ? value : 4;
-
+        else if (k == "track_graphs")
+            ctx->track_graphs_on = value != 0;
         else if (k == "fwd_wave")
             ctx->fwd_wave = value > 0 ? value : 8;
         else
@@ -1152,7 +1211,7 @@ void finish_codeset(tdg_ctx* ctx, tdg_codeset* cs, const float* d, const float* 
     for (uint64_t i = 0; i < n; ++i)
         sd[i] = {d + i * stride, u ? u + i * stride : nullptr, lens[i], cs->rep.as<float>() + i * cs->rep_cap,
                  cs->rep_cap, cs->nlen_dev.as<uint64_t>() + i, cs->energy_dev.as<float>() + i, cs->abs_dev.as<float>() + i};
-    auto* sdd = ctx->upload(ctx->pk_stats, sd);
+    auto* sdd = ctx->upload(ctx->pk->stats, sd);
     tdg::k_support<<<unsigned(n), 1024, 0, ctx->stream>>>(sdd);
     LAUNCHED();
     cs->nlen.resize(n);
@@ -1194,7 +1253,7 @@ void demod_launch(tdg_ctx* ctx, const void* in, bool int16_input, uint64_t in_le
     const int V = 1024 - (ctx->clen - 1);
     const uint64_t nblocks = (W + uint64_t(V) - 1) / uint64_t(V);
     const float2* tw = ctx->twiddles(1024);
-    auto* wd = ctx->upload(ctx->pk_misc, wins);
+    auto* wd = ctx->upload(ctx->pk->misc, wins);
     KScope ks(ctx, "demod");
     // launches that leave the SMs mostly idle take the two-warps-per-block
     // variant (shorter per-warp chain, one more forward transform per block)
@@ -1203,8 +1262,9 @@ void demod_launch(tdg_ctx* ctx, const void* in, bool int16_input, uint64_t in_le
         dim3 grid(unsigned((nblocks + uint64_t(nblk) - 1) / uint64_t(nblk)), unsigned(wins.size()));
         const size_t sm = size_t(nblk * warps_per_blk) * (32 * 33) * sizeof(float2) + size_t(nblk) * 1024 * sizeof(float);
         set_smem(kern, sm);
-        kern<<<grid, nblk * warps_per_blk * 32, sm, ctx->stream>>>(src, in_len, wd, uint32_t(W), ctx->clen, n_bins,
-                                                                  slot_stride, H, eps, tw, ring_cap);
+        if (STREAM_OPS)
+            kern<<<grid, nblk * warps_per_blk * 32, sm, ctx->stream>>>(src, in_len, wd, uint32_t(W), ctx->clen, n_bins,
+                                                                      slot_stride, H, eps, tw, ring_cap);
     };
     if (int16_input) {
         const auto* src = static_cast<const int32_t*>(in);
@@ -1478,7 +1538,7 @@ void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float thre
             x.code_index = int32_t(c);
             x.bin = int32_t(s % w->n_bins);
         }
-    auto* sdd = ctx->upload(ctx->pk_stats, sd);
+    auto* sdd = ctx->upload(ctx->pk->stats, sd);
     {
         // correlation stage incl. the forward transforms it overlaps (those are
         // also timed on their own as fwd_pass1/2)
@@ -1609,7 +1669,7 @@ void track_impl(tdg_ctx* ctx, const tdg_demod_config* cfg, const SampleSource& s
     // keys[i]: argmax of task i; keys[n_tasks]: sink for the stored pair's
     // other code (its correlation comes for free in the packed IFFT)
     ctx->keys.ensure((n_tasks + 1) * sizeof(unsigned long long));
-    CK(cudaMemsetAsync(ctx->keys.p, 0, (n_tasks + 1) * sizeof(unsigned long long), ctx->stream));
+    if (STREAM_OPS) CK(cudaMemsetAsync(ctx->keys.p, 0, (n_tasks + 1) * sizeof(unsigned long long), ctx->stream));
     unsigned long long* keys = ctx->keys.as<unsigned long long>();
     std::vector<CorrJob> jobs(n_tasks);
     for (uint64_t i = 0; i < n_tasks; ++i) {
@@ -1634,13 +1694,116 @@ void track_impl(tdg_ctx* ctx, const tdg_demod_config* cfg, const SampleSource& s
         x.code_index = int32_t(c);
         x.bin = 0;
     }
-    auto* sdd = ctx->upload(ctx->pk_stats, sd);
+    auto* sdd = ctx->upload(ctx->pk->stats, sd);
     launch_stats(ctx, sdd, n_tasks, uint32_t(W), cfg->mod.sample_rate, threshold);
     if (out) {
         CK(cudaMemcpyAsync(out, ctx->det_dev.p, n_tasks * sizeof(tdg_detection), cudaMemcpyDeviceToHost,
                            ctx->stream));
         if (sync) CK(cudaStreamSynchronize(ctx->stream));
     }
+}
+
+// Synchronous tracking of a linear sample block: batches that fit one
+// correlation wave run as CUDA graphs once seen twice with the same key
+// (first call: normal, warming every cache; second: captured; later: the
+// host rebuilds the descriptors in the graph's staging and launches it).
+// Larger batches, or any buffer move in between, take the normal path.
+void track_linear(tdg_ctx* ctx, const tdg_demod_config* cfg, const SampleSource& src, const tdg_track_task* tasks,
+                  uint64_t n_tasks, const tdg_codeset* cs, float threshold, tdg_detection* out) {
+    const uint64_t wave = uint64_t(std::max<int64_t>(tdg::kGroup, ctx->wave_pairs / tdg::kGroup * tdg::kGroup));
+    if (!ctx->track_graphs_on || n_tasks > wave) {
+        track_impl(ctx, cfg, src, tasks, n_tasks, cs, threshold, out);
+        return;
+    }
+    const tdg_modulation& m = cfg->mod;
+    // (the tasks and stream_start only enter descriptor contents, rebuilt on
+    // every call; tdg_set_option drops every graph)
+    const std::vector<double> key{double(n_tasks),       double(cs->window_len), double(src.len),
+                                  double(threshold),     m.sample_rate,          m.bit_rate,
+                                  m.freq_one,            m.freq_zero,            double(m.packet_bits),
+                                  cfg->lo_freq,          cfg->bandpass_center,   cfg->bandpass_width,
+                                  double(cfg->bandpass_taps), double(cfg->eps)};
+    TrackGraph* g = nullptr;
+    for (auto& x : ctx->track_graphs)
+        if (x->cs == cs && x->base == src.base && x->key == key) g = x.get();
+    const uint64_t ep = g_dev_epoch.load();
+    auto finish = [&] {
+        if (out) CK(cudaMemcpyAsync(out, ctx->det_dev.p, n_tasks * sizeof(tdg_detection), cudaMemcpyDeviceToHost,
+                                    ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    };
+    // host pass in graph mode `mode` with the entry's staging; always restores
+    auto host_pass = [&](int mode) {
+        tl_graph_mode = mode;
+        ctx->pk = &g->packs;
+        try {
+            track_impl(ctx, cfg, src, tasks, n_tasks, cs, threshold, nullptr, false);
+        } catch (...) {
+            tl_graph_mode = 0;
+            ctx->pk = &ctx->own_packs;
+            throw;
+        }
+        tl_graph_mode = 0;
+        ctx->pk = &ctx->own_packs;
+    };
+    if (g && g->state == 2 && g->epoch == ep) {
+        g->last_use = ++ctx->graph_clock;
+        host_pass(2);
+        if (g_dev_epoch.load() == ep) {
+            CK(cudaGraphLaunch(g->exec, ctx->stream));
+            LAUNCHED_GRAPH();
+            finish();
+            return;
+        }
+        g->state = 0;   // something moved during the host pass
+    } else if (g && g->state == 1 && g->epoch == ep) {
+        g->last_use = ++ctx->graph_clock;
+        host_pass(2);   // validates the batch and sizes the entry's staging (its only allocations)
+        const uint64_t ep2 = g_dev_epoch.load();
+        cudaGraph_t graph = nullptr;
+        bool ok = cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            try {
+                host_pass(1);
+            } catch (...) {
+                ok = false;
+            }
+            ok = cudaStreamEndCapture(ctx->stream, &graph) == cudaSuccess && ok && graph;
+        }
+        if (g->exec) cudaGraphExecDestroy(g->exec);
+        g->exec = nullptr;
+        ok = ok && cudaGraphInstantiate(&g->exec, graph, 0) == cudaSuccess;
+        if (graph) cudaGraphDestroy(graph);
+        if (ok && g_dev_epoch.load() == ep2) {
+            g->state = 2;
+            g->epoch = ep2;
+            CK(cudaGraphLaunch(g->exec, ctx->stream));
+            LAUNCHED_GRAPH();
+            finish();
+            return;
+        }
+        // not capturable: this key stays on the stream path (same kernels)
+        cudaGetLastError();
+        g->state = -1;
+        track_impl(ctx, cfg, src, tasks, n_tasks, cs, threshold, out);
+        return;
+    }
+    track_impl(ctx, cfg, src, tasks, n_tasks, cs, threshold, out);
+    if (!g) {
+        if (ctx->track_graphs.size() >= 8) {   // evict the least recently used entry
+            auto lru = std::min_element(ctx->track_graphs.begin(), ctx->track_graphs.end(),
+                                        [](const auto& a, const auto& b) { return a->last_use < b->last_use; });
+            ctx->track_graphs.erase(lru);
+        }
+        ctx->track_graphs.push_back(std::make_unique<TrackGraph>());
+        g = ctx->track_graphs.back().get();
+        g->cs = cs;
+        g->base = src.base;
+    }
+    g->key = key;
+    if (g->state != -1) g->state = 1;
+    g->last_use = ++ctx->graph_clock;
+    g->epoch = g_dev_epoch.load();
 }
 }  // namespace
 
@@ -1650,7 +1813,8 @@ int tdg_track_device(tdg_ctx* ctx, const tdg_demod_config* cfg, const int16_t* i
     return guard([&] {
         CK(cudaSetDevice(ctx->device));
         if (n_tasks == 0) return;
-        track_impl(ctx, cfg, SampleSource::linear(iq_dev, n_complex, stream_start), tasks, n_tasks, cs, threshold, out);
+        track_linear(ctx, cfg, SampleSource::linear(iq_dev, n_complex, stream_start), tasks, n_tasks, cs, threshold,
+                     out);
     });
 }
 
@@ -1663,8 +1827,8 @@ int tdg_track(tdg_ctx* ctx, const tdg_demod_config* cfg, const int16_t* iq, uint
         ctx->stream_buf.ensure(n_complex * 2 * sizeof(int16_t));
         CK(cudaMemcpyAsync(ctx->stream_buf.p, iq, n_complex * 2 * sizeof(int16_t), cudaMemcpyHostToDevice,
                            ctx->stream));
-        track_impl(ctx, cfg, SampleSource::linear(ctx->stream_buf.as<int16_t>(), n_complex, stream_start), tasks, n_tasks,
-                   cs, threshold, out);
+        track_linear(ctx, cfg, SampleSource::linear(ctx->stream_buf.as<int16_t>(), n_complex, stream_start), tasks,
+                     n_tasks, cs, threshold, out);
     });
 }
 

@@ -372,6 +372,47 @@ def test_tracking_batch_parity(gpu_ctx, ref):
     assert dets[6]["partial"] and not dets[6]["accepted"]
 
 
+def test_tracking_graph_replay_bitwise(ref):
+    """Small tracking batches are replayed as CUDA graphs from the third call
+    with the same shape (warm, capture, replay): every record must be bitwise
+    equal to the stream path's, across changing tasks, interleaved batch
+    sizes, a rejected batch and a code set rebuilt in between."""
+    from paper_2005_10445_b200 import capi
+    from paper_2005_10445_b200._abi import demod_config
+    cfg = demod_config()
+    fs = cfg.mod.sample_rate
+    W = 96000
+    seeds = [2100 + i for i in range(4)]
+    bits = np.stack([ref.gen_code(s, cfg) for s in seeds])
+    inj = [(0, 0.0103, 1.0, 0.0), (2, 0.0412, 0.8, 0.0), (3, 0.0707, 1.0, 0.0)]
+    iq = ref.generate_recording(cfg, seeds, 0.1, 10.0, 78, inj)
+    toas = [int(round(t * fs)) for _, t, _, _ in inj]
+    rng = np.random.default_rng(5)
+    batches = []
+    for k in range(6):
+        nb = 3 if k % 3 != 2 else 2
+        starts = [int(toas[(k + i) % 3] - 16000 + rng.integers(-3000, 3000)) for i in range(nb)]
+        codes = [int((k + i) % 4) for i in range(nb)]
+        batches.append((starts, codes))
+    with capi.Context(0) as ctx:
+        cs = capi.CodeSet.prepare(ctx, cfg, W, bits)
+        ctx.set_option("track_graphs", 0)
+        want = [capi.track(ctx, cfg, iq, st, co, cs, 0.25) for st, co in batches]
+        ctx.set_option("track_graphs", 1)
+        for rep in range(3):
+            for (st, co), w in zip(batches, want):
+                got = capi.track(ctx, cfg, iq, st, co, cs, 0.25)
+                assert got.tobytes() == w.tobytes(), (rep, st, co)
+            if rep == 0:
+                with pytest.raises(capi.InvalidArgument):
+                    capi.track(ctx, cfg, iq, [10], [len(bits)], cs, 0.25)
+            if rep == 1:
+                # a rebuilt code set moves buffers: graphs must not replay stale pointers
+                cs.close()
+                cs = capi.CodeSet.prepare(ctx, cfg, W, bits)
+        assert want[0]["accepted"].any()
+
+
 def test_tracking_rejects_bad_tasks(gpu_ctx):
     from paper_2005_10445_b200 import capi
     from paper_2005_10445_b200._abi import desk_config

@@ -53,11 +53,13 @@ def main():
               (B, label, np.median(ts) * 1e6, np.min(ts) * 1e6, np.median(gs)))
 
     measure("default")
-    for key, val in [("one_stream", 1), ("n_streams", 1)]:
+    for key, val in [("track_graphs", 0), ("one_stream", 1), ("n_streams", 1)]:
         ctx.set_option(key, val)
         measure("%s=%d" % (key, val))
+    ctx.set_option("track_graphs", 1)
     ctx.set_option("one_stream", 0)
     ctx.set_option("n_streams", 2)
+    measure("default")
     ctx.set_option("time_kernels", 1)
     ctx.kernel_time_reset()
     for _ in range(50):
