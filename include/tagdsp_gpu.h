@@ -176,7 +176,11 @@ int tdg_track_ring(tdg_ctx* ctx, tdg_ring* ring, const tdg_demod_config* cfg, co
 /* Tuning / profiling knobs (0 = default): "wave_pairs", "ring", "n_streams",
  * "discard", "fwd_wave", "one_stream", "cta_cap_a", "cta_cap_b",
  * "time_kernels" (1 = record a CUDA event pair on the context stream around
- * every launch; read back with tdg_kernel_time). */
+ * every launch; read back with tdg_kernel_time), "track_graphs" (default 1:
+ * tdg_track / tdg_track_device batches that fit one correlation wave are
+ * captured as a CUDA graph on their second call with the same shape and
+ * replayed from the third; 0 = always issue the launches).  Setting any
+ * option drops the context's captured graphs. */
 int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value);
 /* Launch count and summed device time (ms) of one kernel family since the
  * last reset: "demod", "fwd_pass1", "fwd_pass2", "corr_passA", "corr_passB",
