@@ -27,7 +27,9 @@ from ._abi import (DETECTION_DTYPE, TRACK_TASK_DTYPE, DemodConfig, RingPushResul
                    desk_config)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtagdsp_gpu.so")
+# TDG_LIB_PATH: load another build of the same library (A/B timing of
+# compile-time variants with tools/; still the CUDA path, never a fallback)
+LIB_PATH = os.environ.get("TDG_LIB_PATH") or os.path.join(_HERE, "libtagdsp_gpu.so")
 
 TDG_OK, TDG_EINVAL, TDG_ECUDA, TDG_ENOMEM, TDG_ERANGE, TDG_EINTERNAL = range(6)
 
