@@ -417,16 +417,6 @@ def main():
         barrier()
         torch.cuda.cudart().cudaProfilerStop()
 
-    # ---- per-kernel CUDA events (same steps, separate pass: recording an
-    # event pair around each of ~800 launches perturbs the step time) -------
-    ctx.kernel_time_reset()
-    ctx.set_option("time_kernels", 1)
-    for _ in range(args.steps):
-        step_device()
-    barrier()
-    kt = {k: ctx.kernel_time(k) for k in ("demod", "fwd_pass1", "fwd_pass2", "corr", "stats")}
-    ctx.set_option("time_kernels", 0)
-
     # ---- end-to-end through the C-ABI from pinned host memory ----------------
     for _ in range(args.warmup):
         step_e2e()
@@ -440,6 +430,16 @@ def main():
     e2e_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     wall_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / args.steps)
     e2e = n_units * world / (e2e_ms / 1e3)
+
+    # ---- per-kernel CUDA events (same steps, separate pass: recording an
+    # event pair around each of ~800 launches perturbs the step time) -------
+    ctx.kernel_time_reset()
+    ctx.set_option("time_kernels", 1)
+    for _ in range(args.steps):
+        step_device()
+    barrier()
+    kt = {k: ctx.kernel_time(k) for k in ("demod", "fwd_pass1", "fwd_pass2", "corr", "stats")}
+    ctx.set_option("time_kernels", 0)
 
     # ---- roofline of the dominant stage: the correlation engine -------------
     # (k_corr_pass pass A + pass B on two streams, one per-step event pair)
