@@ -22,6 +22,7 @@ host threads) on a bounded sample of the same workload.
 """
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -472,6 +473,12 @@ def main():
         # n_gpus codes) x 9 bins: N_WIN windows x advance per step
         "real_time_factor": (N_WIN * ADV / FS) / (ms_max / 1e3),
         "real_time_factor_e2e": (N_WIN * ADV / FS) / (e2e_ms / 1e3),
+        # the paper's figures (proj/src/harness.cpp:15-25): perf_ratio = time
+        # per pattern (one code against one window, here per bin) / window
+        # duration, and the patterns one GPU keeps up with in real time
+        # (search_share 1) = floor(1 / perf_ratio); from the e2e time
+        "paper_perf_ratio": (e2e_ms / 1e3 / n_units) / (W / FS),
+        "paper_throughput_patterns": int(math.floor(1.0 / ((e2e_ms / 1e3 / n_units) / (W / FS)))),
         "e2e": {"value": e2e, "unit": "corr/s", "ms_per_step": e2e_ms, "wall_ms_per_step": wall_ms,
                 "h2d_bytes_per_step": int(iq.nbytes), "d2h_bytes_per_step": int(n_units * DETECTION_DTYPE.itemsize),
                 "path": "streaming C-ABI: tdg_ring_push (pinned host int16 -> device CircularBuffer, copy "
