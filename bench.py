@@ -199,6 +199,8 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (FFT in f64 shim)",
         "data": "synthetic", "config": workload_config(world),
         "real_time_factor": (N_WIN * ADV / FS) / (N_CODES * len(BINS) * N_WIN / val),
+        "paper_perf_ratio": (1.0 / val) / (W / FS),
+        "paper_throughput_patterns": int(math.floor(val * (W / FS))),
         "cpu_baseline": {"value": val, "unit": "corr/s", "cores": threads, "kind": "reference", "sample": sample,
                          "fft": "oracle/fftw_shim (no libfftw3f on the box)"},
         "e2e": {"value": val, "unit": "corr/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
