@@ -201,6 +201,7 @@ def run_reference(args):
         "real_time_factor": (N_WIN * ADV / FS) / (N_CODES * len(BINS) * N_WIN / val),
         "paper_perf_ratio": (1.0 / val) / (W / FS),
         "paper_throughput_patterns": int(math.floor(val * (W / FS))),
+        "paper_tags_searchable_50pct": int(math.floor(0.5 * val * (W / FS))),
         "cpu_baseline": {"value": val, "unit": "corr/s", "cores": threads, "kind": "reference", "sample": sample,
                          "fft": "oracle/fftw_shim (no libfftw3f on the box)"},
         "e2e": {"value": val, "unit": "corr/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -481,6 +482,9 @@ def main():
         # (search_share 1) = floor(1 / perf_ratio); from the e2e time
         "paper_perf_ratio": (e2e_ms / 1e3 / n_units) / (W / FS),
         "paper_throughput_patterns": int(math.floor(1.0 / ((e2e_ms / 1e3 / n_units) / (W / FS)))),
+        # PAPER Table 3's column (search_share 0.5): 6 / 26 / 77 / 315 tags on
+        # i7-8700T / Jetson TX2 / GTX 1050 / Titan Xp
+        "paper_tags_searchable_50pct": int(math.floor(0.5 / ((e2e_ms / 1e3 / n_units) / (W / FS)))),
         "e2e": {"value": e2e, "unit": "corr/s", "ms_per_step": e2e_ms, "wall_ms_per_step": wall_ms,
                 "h2d_bytes_per_step": int(iq.nbytes), "d2h_bytes_per_step": int(n_units * DETECTION_DTYPE.itemsize),
                 "path": "streaming C-ABI: tdg_ring_push (pinned host int16 -> device CircularBuffer, copy "
