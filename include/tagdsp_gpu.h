@@ -64,7 +64,9 @@ uint64_t tdg_corr_len(uint64_t window_len, uint64_t nonzero_len);
  * with lo_freq = 0 (proj/src/dsp.cpp:159-191) -> support / energy / abs_sum
  * (proj/src/detector.cpp:20-43) -> forward FFT of the zero-padded replica d
  * (:45-47).  bits is n_codes x cfg->mod.packet_bits bytes (0/1).
- * Errors as the reference: window_len < packet_samples -> TDG_EINVAL. */
+ * Errors as the reference: window_len < packet_samples -> TDG_EINVAL;
+ * beyond the reference: window_len + support - 1 > 1,048,576 (the largest
+ * instantiated transform, tdg_corr_len() == 0) -> TDG_ERANGE. */
 int tdg_codeset_prepare(tdg_ctx* ctx, const tdg_demod_config* cfg, uint64_t window_len,
                         const uint8_t* bits, uint64_t n_codes, tdg_codeset** out);
 /* make_transformed (proj/src/detector.cpp:11-48) from host replicas:
