@@ -324,6 +324,10 @@ def test_invalid_arguments_raise(gpu_ctx):
         capi.detect(gpu_ctx, w, cs)                               # mixed window shapes
     with pytest.raises(capi.InvalidArgument):
         capi.demodulate_window(gpu_ctx, np.zeros(3, np.int16), 0, cfg)   # odd raw count
+    # beyond the largest instantiated transform (1024 x 1024): a clear error, no launch
+    assert capi.corr_len(1 << 20, 2) == 0
+    with pytest.raises(capi.GpuError, match="largest supported transform"):
+        capi.CodeSet.from_replicas(gpu_ctx, 1 << 20, (1 << 20) + 100, [np.ones(64, np.float32)])
 
 
 def test_tracking_batch_parity(gpu_ctx, ref):
