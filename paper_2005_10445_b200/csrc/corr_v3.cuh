@@ -452,12 +452,17 @@ __global__ void __launch_bounds__(128, 3) k_corr_pass(const __grid_constant__ Co
             item_passA<PA, QA, PB, QB>(S, D, k, sl, prefetch);
         } else {
             // the M tile is in shared memory and its L2 lines are dead: drop
-            // them without a DRAM write-back (ordered before the ring slot's
-            // reuse by the kernel boundary)
+            // them without a DRAM write-back.  Only lines wholly inside the
+            // tile: a tile that does not start on a 128-byte line (N1 * 32
+            // bytes not a multiple of 128, e.g. N1 = 450) shares its edge lines
+            // with the neighbouring tiles, whose items may not have read them yet.
             const CorrPairOut& po = D.outs[k.idx / S.n_tiles];
-            const char* tile = reinterpret_cast<const char*>(po.M + size_t(k.idx % S.n_tiles) * F::LB * kTileB);
+            const uintptr_t t0 = reinterpret_cast<uintptr_t>(po.M + size_t(k.idx % S.n_tiles) * F::LB * kTileB);
+            const uintptr_t lo = (t0 + 127) & ~uintptr_t(127);
+            const uintptr_t hi = (t0 + uintptr_t(F::LB) * kTileB * 8) & ~uintptr_t(127);
             if (S.discard)
-                for (int l = threadIdx.x; l < F::LB * kTileB * 8 / 128; l += F::NT) discard_l2(tile + size_t(l) * 128);
+                for (uintptr_t a = lo + uintptr_t(threadIdx.x) * 128; a < hi; a += uintptr_t(F::NT) * 128)
+                    discard_l2(reinterpret_cast<const void*>(a));
             item_passB<PA, QA, PB, QB>(S, D, k, sl);
         }
         __syncthreads();   // slot s consumed (pass A: its staged columns complete)

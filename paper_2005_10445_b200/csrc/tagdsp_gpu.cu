@@ -107,6 +107,11 @@ struct DevBuf {
         CK(cudaMalloc(&p, b));
         g_dev_epoch.fetch_add(1, std::memory_order_relaxed);
         bytes = b;
+        // debugging aid: TDG_POISON_ALLOC=<byte> fills new device buffers with
+        // that byte (0x7f: +3.4e38 floats, 0xff: NaN), so a read before the
+        // first write shows up in the results
+        static const int poison = getenv("TDG_POISON_ALLOC") ? int(strtol(getenv("TDG_POISON_ALLOC"), nullptr, 0)) : -1;
+        if (poison >= 0) CK(cudaMemset(p, poison, b));
     }
     template <class T>
     T* as() const { return static_cast<T*>(p); }
@@ -195,8 +200,9 @@ const PassShape& shape_of(int L) {
     fail(TDG_ERANGE, "unsupported pass length %d", L);
 }
 
-constexpr int kTB = 8;   // t2 columns per CTA in the chunked passes (F1, B)
-constexpr int kG = 2;    // code pairs per pass-A work item
+// forward pass 1: t2 columns per CTA -- as many as keep a CTA's transpose
+// tile within 160 KB (wider tiles: longer coalesced runs per load row)
+constexpr int fwd1_tb(int L) { return size_t(L) * 32 * sizeof(float2) <= 160 * 1024 ? 32 : 16; }
 constexpr int kDemodBlk = 4;
 
 uint64_t pad_length_impl(uint64_t n) {
@@ -293,13 +299,15 @@ int block_for(int tasks) {
     return std::min(256, std::max(32, t));
 }
 
-void launch_fwd1(int L, dim3 grid, cudaStream_t st, const tdg::SeqPairDesc* pairs, int N2, const float2* tw) {
+void launch_fwd1(int L, unsigned n_seq, cudaStream_t st, const tdg::SeqPairDesc* pairs, int N2, const float2* tw) {
     switch (L) {
 #define X(LL, P, Q)                                                                        \
     case LL: {                                                                             \
-        const size_t sm = size_t(P) * Q * kTB * sizeof(float2);                            \
-        set_smem(tdg::k_fwd_pass1<P, Q, kTB>, sm);                                         \
-        if (STREAM_OPS) tdg::k_fwd_pass1<P, Q, kTB><<<grid, block_for(std::max(P, Q) * kTB), sm, st>>>(pairs, N2, tw); \
+        constexpr int TB = fwd1_tb(LL);                                                    \
+        const size_t sm = size_t(P) * Q * TB * sizeof(float2);                             \
+        const dim3 grid(unsigned((N2 + TB - 1) / TB), n_seq);                              \
+        set_smem(tdg::k_fwd_pass1<P, Q, TB>, sm);                                          \
+        if (STREAM_OPS) tdg::k_fwd_pass1<P, Q, TB><<<grid, block_for(std::max(P, Q) * TB), sm, st>>>(pairs, N2, tw); \
         LAUNCHED();                                                                        \
         return;                                                                            \
     }
@@ -843,7 +851,7 @@ void run_forward(tdg_ctx* ctx, int N1, int N2, const std::vector<FwdJob>& jobs, 
         const size_t n = std::min(wave, jobs.size() - base);
         {
             KScope ks(ctx, "fwd_pass1");
-            launch_fwd1(N1, dim3(unsigned((N2 + kTB - 1) / kTB), unsigned(n)), ctx->stream, dd + base, N2, tw1);
+            launch_fwd1(N1, unsigned(n), ctx->stream, dd + base, N2, tw1);
         }
         {
             KScope ks(ctx, "fwd_pass2");

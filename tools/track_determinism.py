@@ -47,6 +47,19 @@ def main():
                     capi.track(ctx, cfg, iq, [10], [len(bits)], cs, 0.25)
                 except capi.InvalidArgument:
                     print("bad batch rejected", flush=True)
+    # first call on a fresh context against later calls (reads of memory
+    # before its first write differ between the two)
+    for trial in range(3):
+        with capi.Context(0) as ctx:
+            cs = capi.CodeSet.prepare(ctx, cfg, W, bits)
+            ctx.set_option("track_graphs", 0)
+            first = capi.track(ctx, cfg, iq, st, co, cs, 0.25)
+            for b in batches:
+                capi.track(ctx, cfg, iq, b[0], b[1], cs, 0.25)
+            later = capi.track(ctx, cfg, iq, st, co, cs, 0.25)
+            print("fresh-context trial %d: first %s later %s %s" % (
+                trial, list(first["peak_index"]), list(later["peak_index"]),
+                "same" if first.tobytes() == later.tobytes() else "DIFFERENT"), flush=True)
     with capi.Context(0) as ctx:
         cs = capi.CodeSet.prepare(ctx, cfg, W, bits)
         for graphs in (0, 1):
