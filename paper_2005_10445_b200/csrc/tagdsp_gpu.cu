@@ -200,9 +200,10 @@ const PassShape& shape_of(int L) {
     fail(TDG_ERANGE, "unsupported pass length %d", L);
 }
 
-// forward pass 1: t2 columns per CTA -- as many as keep a CTA's transpose
-// tile within 160 KB (wider tiles: longer coalesced runs per load row)
-constexpr int fwd1_tb(int L) { return size_t(L) * 32 * sizeof(float2) <= 160 * 1024 ? 32 : 16; }
+// forward pass 1: t2 columns per CTA (16: 64-byte runs per load row; 8 was
+// ~10 % slower on tracking batches, 32 where it fits ~1 % slower than 16,
+// tools/ab_libs.sh)
+constexpr int fwd1_tb(int) { return 16; }
 constexpr int kDemodBlk = 4;
 
 uint64_t pad_length_impl(uint64_t n) {
