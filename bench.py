@@ -39,6 +39,7 @@ ADV = 720000
 BINS = np.arange(-400e3, 400e3 + 1.0, 100e3)
 DURATION = 1.0
 FS = 8.0e6
+WAVE_PAIRS = 12   # the library's default correlation wave (tdg_set_option "wave_pairs")
 N_WIN = int((DURATION * FS - W) // ADV) + 1          # 11
 CORR_LEN = 870912
 NONZERO = 65741
@@ -446,7 +447,7 @@ def main():
     ctx.set_option("time_kernels", 0)
 
     # ---- roofline of the dominant stage: the correlation engine -------------
-    # (k_corr_pass pass A + pass B on two streams, one per-step event pair)
+    # (k_corr_pass pass A + pass B on overlapped streams, one per-step event pair)
     pk = peaks()
     n_corr_launch, ms_corr = kt["corr"]
     corr_ms_step = ms_corr / max(1, n_corr_launch)
@@ -494,7 +495,9 @@ def main():
         "roofline": {"bound": "hbm",
                      "kernel": "correlation engine per step: k_corr_pass<27,32,32,32,0> (spectral product + "
                                "first inverse-FFT pass) and k_corr_pass<...,1> (second pass + argmax), "
-                               "%d launches on two overlapped streams" % (2 * (((n_codes + 1) // 2 * N_WIN * len(BINS) + 7) // 8)),
+                               "%d launches in waves of %d pairs over 4 pass-A + 4 pass-B streams" % (
+                                   2 * (((n_codes + 1) // 2 * N_WIN * len(BINS) + WAVE_PAIRS - 1) // WAVE_PAIRS),
+                                   WAVE_PAIRS),
                      "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
                      "traffic": traffic, "peak_source": pk["source"],
                      "traffic_note": "dram__bytes_read+write of all correlation launches of one step, warm L2 "

@@ -515,7 +515,7 @@ struct tdg_ctx {
     std::vector<cudaEvent_t> ev_a, ev_b;
     std::vector<cudaStream_t> a_streams, b_streams;
     std::vector<cudaEvent_t> ev_fwd;                  // forward-transform waves done
-    int64_t n_streams = 2;
+    int64_t n_streams = 4;
     void ensure_pipeline(int ring) {   // (set_option("n_streams") drops the old streams)
         const size_t ns = size_t(std::max<int64_t>(1, std::min<int64_t>(n_streams, 8)));
         while (a_streams.size() < ns) {
@@ -1183,7 +1183,7 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
             for (auto x : ctx->b_streams) CK(cudaStreamDestroy(x));
             ctx->a_streams.clear();
             ctx->b_streams.clear();
-            ctx->n_streams = value > 0 ? value : 2;
+            ctx->n_streams = value > 0 ? value : 4;
         } else if (k == "cta_cap_a")
             g_cta_cap[0] = int(value);
         else if (k == "cta_cap_b")
