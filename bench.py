@@ -39,7 +39,7 @@ ADV = 720000
 BINS = np.arange(-400e3, 400e3 + 1.0, 100e3)
 DURATION = 1.0
 FS = 8.0e6
-WAVE_PAIRS = 12   # the library's default correlation wave (tdg_set_option "wave_pairs")
+WAVE_PAIRS = 8    # the library's default correlation wave (tdg_set_option "wave_pairs")
 N_WIN = int((DURATION * FS - W) // ADV) + 1          # 11
 CORR_LEN = 870912
 NONZERO = 65741
@@ -342,6 +342,11 @@ def main():
     n_codes = len(bits)
     n_complex = iq.size // 2
     ctx = capi.Context(local)
+    # TDG_BENCH_OPTIONS="wave_pairs=10,n_streams=4": tuning knobs for sweeps
+    # (tdg_set_option); the default run sets none
+    for kv in filter(None, os.environ.get("TDG_BENCH_OPTIONS", "").split(",")):
+        k, v = kv.split("=")
+        ctx.set_option(k, int(v))
     cs = capi.CodeSet.prepare(ctx, cfg, W, bits)
     corr_len_used = cs.info(0)["corr_len"]
     win = capi.Windows(ctx, W, N_WIN, len(BINS))

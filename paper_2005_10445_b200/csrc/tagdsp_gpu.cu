@@ -548,7 +548,7 @@ struct tdg_ctx {
     int64_t track_graphs_on = 1;   // small tracking batches replayed as CUDA graphs
     uint64_t graph_clock = 0;
     std::vector<char> host_stage;
-    int64_t wave_pairs = 12;     // correlation pairs per wave (one pass-A + one pass-B launch)
+    int64_t wave_pairs = 8;      // correlation pairs per wave (one pass-A + one pass-B launch)
     int64_t ring = 4;            // M wave buffers in flight
     int64_t discard = 1;         // drop consumed M tiles from L2
     int64_t one_stream = 0;      // tuning: run pass B on the context stream too (no overlap)
@@ -1176,7 +1176,7 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
             ctx->collect();
             ctx->time_kernels = value != 0;
         } else if (k == "wave_pairs")
-            ctx->wave_pairs = value > 0 ? value : 12;
+            ctx->wave_pairs = value > 0 ? value : 8;
         else if (k == "n_streams") {
             CK(cudaDeviceSynchronize());
             for (auto x : ctx->a_streams) CK(cudaStreamDestroy(x));
