@@ -111,7 +111,10 @@ struct DevBuf {
         // that byte (0x7f: +3.4e38 floats, 0xff: NaN), so a read before the
         // first write shows up in the results
         static const int poison = getenv("TDG_POISON_ALLOC") ? int(strtol(getenv("TDG_POISON_ALLOC"), nullptr, 0)) : -1;
-        if (poison >= 0) CK(cudaMemset(p, poison, b));
+        if (poison >= 0) {   // complete before any stream (non-blocking ones included) writes it
+            CK(cudaMemset(p, poison, b));
+            CK(cudaDeviceSynchronize());
+        }
     }
     template <class T>
     T* as() const { return static_cast<T*>(p); }

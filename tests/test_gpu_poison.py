@@ -23,4 +23,5 @@ def test_parity_with_poisoned_allocations(byte):
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
                         os.path.join(HERE, "test_gpu_parity.py"), os.path.join(HERE, "test_gpu_ring.py")],
                        env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-2000:])
+    failed = [l for l in r.stdout.splitlines() if l.startswith(("FAILED", "ERROR", "E "))]
+    assert r.returncode == 0, ("\n".join(failed[:40]), r.stderr[-2000:])
