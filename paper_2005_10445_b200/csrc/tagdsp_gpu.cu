@@ -195,7 +195,6 @@ const PassShape kMenu[] = {
     TDG_MENU(X)
 #undef X
 };
-constexpr int kMenuN = sizeof(kMenu) / sizeof(kMenu[0]);
 
 const PassShape& shape_of(int L) {
     for (const auto& s : kMenu)
