@@ -49,10 +49,13 @@ struct Fused {
     static constexpr int LA = PA * QA, LB = PB * QB;
     static constexpr int QSA = qstride_even_pad(QA);
     static constexpr int TWS = inter_tw_stride(PA, QA);
-    // pass-A slot: [D column][X columns: 2 per pair][transpose reuses D/X] [2 twiddle rows]
-    // per-warp transpose / M staging region (128-byte aligned for the TMA store)
+    // pass-A slot: [D column][X columns: 2 per pair][2 twiddle rows], every
+    // column in a region of XS >= the padded transpose, so each warp's
+    // transpose and M staging live over the X column it alone reads (no CTA
+    // barrier inside an item); regions 128-byte aligned for the TMA store
     static constexpr int STG = up16(cmax(PA * QSA, LA));
-    static constexpr int A_OPS = up16(cmax((1 + 2 * kGroup) * LA, kGroup * 2 * STG));
+    static constexpr int XS = STG;
+    static constexpr int A_OPS = (1 + 2 * kGroup) * XS;
     static constexpr int A_SLOT = up16(A_OPS + 2 * TWS);
     static constexpr int ROWB = passb_row(QB);
     static constexpr int B_SLOT = up16(cmax(LB * kTileB, PB * ROWB));
@@ -134,8 +137,8 @@ __device__ __forceinline__ void issue_ticket(const CorrSched& S, const Desc& D, 
         bulk_g2s_hint(sl, gd.D + size_t(cp) * LA, LA * 8, bar, pol_first);
         for (int g = 0; g < gd.npairs; ++g) {
             const float2* X = gd.Ca[g];
-            bulk_g2s_hint(sl + (1 + 2 * g) * LA, X + size_t(self ? cp : F::LB - cp) * LA, LA * 8, bar, pol_last);
-            if (!self) bulk_g2s_hint(sl + (2 + 2 * g) * LA, X + size_t(cp) * LA, LA * 8, bar, pol_last);
+            bulk_g2s_hint(sl + (1 + 2 * g) * F::XS, X + size_t(self ? cp : F::LB - cp) * LA, LA * 8, bar, pol_last);
+            if (!self) bulk_g2s_hint(sl + (2 + 2 * g) * F::XS, X + size_t(cp) * LA, LA * 8, bar, pol_last);
         }
         const int k1b = cp == 0 ? 0 : F::LB - cp;
         bulk_g2s(sl + F::A_OPS, S.twI + size_t(cp) * TWS, TWS * 8, bar);
@@ -178,7 +181,7 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Desc& D, co
     if (act1) {
         const int a = lane;
         const float2* D = sl;
-        const float2* Xm = sl + (1 + 2 * g) * L;   // X column N1-cp (or cp if self)
+        const float2* Xm = sl + (1 + 2 * g) * F::XS;   // X column N1-cp (or cp if self)
         if (col == 0) {
             if (cp == 0) {
 #pragma unroll
@@ -194,7 +197,7 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Desc& D, co
                 }
             }
         } else {
-            const float2* Xc = sl + (2 + 2 * g) * L;  // X column cp
+            const float2* Xc = sl + (2 + 2 * g) * F::XS;  // X column cp
 #pragma unroll
             for (int b = 0; b < Q; ++b) {
                 const int r = (L - 1) - (a + P * b);   // source row of output row a + P*b
@@ -203,18 +206,19 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Desc& D, co
         }
         dft<Q, +1>(v);
     }
-    __syncthreads();  // operands consumed
-    mid();            // thread 0: the next item's bulk copies
+    mid();   // thread 0: the next item's bulk copies (into the other slot)
+    // the transpose goes over this warp's own X column (read only by it)
+    __syncwarp();
     if (act1) {
-        float2* tr = sl + role * F::STG + lane * QS;
+        float2* tr = sl + (1 + role) * F::XS + lane * QS;
 #pragma unroll
         for (int c = 0; c < Q; ++c) tr[c] = v[c];
     }
-    __syncthreads();
+    __syncwarp();
     // ---- step 2: lane c: twiddle, P-point IDFT over a, inter-pass twiddle, store M
     if (act && lane < Q) {
         const int c = lane;
-        const float2* tr = sl + role * F::STG + c;
+        const float2* tr = sl + (1 + role) * F::XS + c;
         float2 w[P];
 #pragma unroll
         for (int a = 0; a < P; ++a) w[a] = tr[a * QS];
@@ -225,7 +229,7 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Desc& D, co
         // stage the column in t2 order in the warp's own region, then one TMA
         // tensor store scatters it into M's tile-major layout (N2/4 chunks of
         // 32 bytes) without occupying the LSU pipe
-        float2* stg = sl + role * F::STG;
+        float2* stg = sl + (1 + role) * F::XS;
         __syncwarp(0xffffffffu >> (32 - Q));   // the region's transposed inputs are consumed
         // w_N^{k1 (c + Q e)} = tc * w_N^{k1 Q e}: exact row values every 8th e,
         // one chained product by w_N^{k1 Q} in between
@@ -257,7 +261,7 @@ __device__ __forceinline__ void store_passA(const CorrSched& S, const Desc& D, c
     const bool self = (cp == 0) || (2 * cp == N1);
     for (int g = 0; g < gd.npairs; ++g)
         for (int col = 0; col < (self ? 1 : 2); ++col)
-            tma_store_4d(&S.mstore, sl + (2 * g + col) * F::STG, 0, col ? N1 - cp : cp, 0, gd.Mi[g]);
+            tma_store_4d(&S.mstore, sl + (1 + 2 * g + col) * F::XS, 0, col ? N1 - cp : cp, 0, gd.Mi[g]);
     bulk_commit();
 }
 
