@@ -417,6 +417,36 @@ def test_tracking_graph_replay_bitwise(ref):
         assert want[0]["accepted"].any()
 
 
+def test_tracking_multiwave_matches_single_tasks(ref):
+    """A batch of 20 tracking tasks (three correlation waves over the four
+    stream pairs) against the same tasks one at a time (single-wave path,
+    CUDA-graph replays from the third): peak indices and flags exact, the
+    statistics equal up to the summation order of the split dot products."""
+    from paper_2005_10445_b200 import capi
+    from paper_2005_10445_b200._abi import demod_config
+    cfg = demod_config()
+    fs = cfg.mod.sample_rate
+    W = 96000
+    seeds = [2200 + i for i in range(6)]
+    bits = np.stack([ref.gen_code(s, cfg) for s in seeds])
+    inj = [(0, 0.0103, 1.0, 0.0), (2, 0.0412, 0.8, 0.0), (5, 0.0707, 1.0, 0.0)]
+    iq = ref.generate_recording(cfg, seeds, 0.1, 10.0, 79, inj)
+    toas = [int(round(t * fs)) for _, t, _, _ in inj]
+    rng = np.random.default_rng(11)
+    starts = [int(toas[i % 3] - 16000 + rng.integers(-4000, 4000)) for i in range(20)]
+    codes = [int(i % 6) for i in range(20)]
+    with capi.Context(0) as ctx:
+        cs = capi.CodeSet.prepare(ctx, cfg, W, bits)
+        batch = capi.track(ctx, cfg, iq, starts, codes, cs, 0.25)
+        singles = np.concatenate([capi.track(ctx, cfg, iq, [s0], [c], cs, 0.25) for s0, c in zip(starts, codes)])
+    for f in ("code_index", "window_start", "peak_index", "accepted", "partial"):
+        assert np.array_equal(batch[f], singles[f]), f
+    for f in ("subsample_offset", "w_c", "q", "p_c", "score", "peak_value"):
+        g, w = batch[f].astype(np.float64), singles[f].astype(np.float64)
+        assert np.all(np.abs(g - w) <= 1e-5 * np.maximum(np.abs(w), 1e-3)), (f, float(np.max(np.abs(g - w))))
+    assert batch["accepted"].sum() >= 3
+
+
 def test_tracking_rejects_bad_tasks(gpu_ctx):
     from paper_2005_10445_b200 import capi
     from paper_2005_10445_b200._abi import desk_config
