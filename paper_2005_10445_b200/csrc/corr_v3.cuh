@@ -1,7 +1,8 @@
 // Correlation engine v3: the two inverse-FFT passes of every (window slot x
 // code pair) correlation as two persistent, TMA-pipelined kernels per wave
-// of `wave_pairs` pairs, issued on two CUDA streams so that pass B of wave w
-// overlaps pass A of wave w+1 (no SM idles in a launch's ramp or tail):
+// of `wave_pairs` pairs, waves alternating over n_streams pass-A and
+// n_streams pass-B CUDA streams so that the passes of neighbouring waves
+// overlap (no SM idles in a launch's ramp or tail):
 //
 //   correlate_spectrum (proj/src/detector.cpp:78-88)  ->  pass A
 //   inverse FFT + find_peak (detector.cpp:122-134)     ->  pass A + pass B
@@ -18,7 +19,9 @@
 // copies (cp.async.bulk -> UBLKCP, completing on an mbarrier) into the
 // second shared-memory slot while the 4 warps run the current item from the
 // first.  Pass-A inter-pass twiddles come from a precomputed table that rides
-// in the same bulk copies, so no item recomputes sincos.
+// in the same bulk copies, so no item recomputes sincos.  In pass A each warp
+// (one column role) transposes and stages over the X column only it reads, so
+// an item has a single CTA barrier (at its end).
 #pragma once
 #include "kernels.cuh"
 #include "tma.cuh"
