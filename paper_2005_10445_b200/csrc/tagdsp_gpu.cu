@@ -554,7 +554,7 @@ struct tdg_ctx {
     int64_t ring = 4;            // M wave buffers in flight
     int64_t discard = 1;         // drop consumed M tiles from L2
     int64_t one_stream = 0;      // tuning: run pass B on the context stream too (no overlap)
-    int64_t fwd_wave = 8;        // sequence pairs per forward-FFT wave
+    int64_t fwd_wave = 32;       // sequence pairs per forward-FFT wave
     // optional per-launch CUDA-event timing (bench.py roofline)
     bool time_kernels = false;
     struct KTime {
@@ -1199,7 +1199,7 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
         else if (k == "track_graphs")
             ctx->track_graphs_on = value != 0;
         else if (k == "fwd_wave")
-            ctx->fwd_wave = value > 0 ? value : 8;
+            ctx->fwd_wave = value > 0 ? value : 32;
         else
             fail(TDG_EINVAL, "unknown option %s", key);
     });
