@@ -514,7 +514,7 @@ def main():
         "roofline": {"bound": "hbm",
                      "kernel": "correlation engine per step: k_corr_pass<27,32,32,32,0> (spectral product + "
                                "first inverse-FFT pass) and k_corr_pass<...,1> (second pass + argmax), "
-                               "%d launches in waves of %d pairs over 4 pass-A + 4 pass-B streams" % (
+                               "%d launches in waves of %d pairs over 6 pass-A + 6 pass-B streams" % (
                                    2 * (((n_codes + 1) // 2 * N_WIN * len(BINS) + WAVE_PAIRS - 1) // WAVE_PAIRS),
                                    WAVE_PAIRS),
                      "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],

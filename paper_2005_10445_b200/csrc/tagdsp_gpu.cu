@@ -517,7 +517,7 @@ struct tdg_ctx {
     std::vector<cudaEvent_t> ev_a, ev_b;
     std::vector<cudaStream_t> a_streams, b_streams;
     std::vector<cudaEvent_t> ev_fwd;                  // forward-transform waves done
-    int64_t n_streams = 4;
+    int64_t n_streams = 6;
     void ensure_pipeline(int ring) {   // (set_option("n_streams") drops the old streams)
         const size_t ns = size_t(std::max<int64_t>(1, std::min<int64_t>(n_streams, 8)));
         while (a_streams.size() < ns) {
@@ -551,7 +551,7 @@ struct tdg_ctx {
     uint64_t graph_clock = 0;
     std::vector<char> host_stage;
     int64_t wave_pairs = 8;      // correlation pairs per wave (one pass-A + one pass-B launch)
-    int64_t ring = 4;            // M wave buffers in flight
+    int64_t ring = 3;            // M wave buffers in flight
     int64_t discard = 1;         // drop consumed M tiles from L2
     int64_t one_stream = 0;      // tuning: run pass B on the context stream too (no overlap)
     int64_t fwd_wave = 32;       // sequence pairs per forward-FFT wave
@@ -1185,7 +1185,7 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
             for (auto x : ctx->b_streams) CK(cudaStreamDestroy(x));
             ctx->a_streams.clear();
             ctx->b_streams.clear();
-            ctx->n_streams = value > 0 ? value : 4;
+            ctx->n_streams = value > 0 ? value : 6;
         } else if (k == "cta_cap_a")
             g_cta_cap[0] = int(value);
         else if (k == "cta_cap_b")
@@ -1195,7 +1195,7 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
         else if (k == "discard")
             ctx->discard = value;
         else if (k == "ring")
-            ctx->ring = value > 0 ? value : 4;
+            ctx->ring = value > 0 ? value : 3;
         else if (k == "track_graphs")
             ctx->track_graphs_on = value != 0;
         else if (k == "fwd_wave")
