@@ -175,8 +175,10 @@ int tdg_search_ring(tdg_ctx* ctx, tdg_ring* ring, const tdg_demod_config* cfg, c
 int tdg_track_ring(tdg_ctx* ctx, tdg_ring* ring, const tdg_demod_config* cfg, const tdg_track_task* tasks,
                    uint64_t n_tasks, const tdg_codeset* cs, float threshold, tdg_detection* out, int sync);
 
-/* Tuning / profiling knobs (0 = default): "wave_pairs", "ring", "n_streams",
- * "discard", "fwd_wave", "one_stream", "cta_cap_a", "cta_cap_b",
+/* Tuning / profiling knobs (0 = default): "wave_pairs" (8), "ring" (3),
+ * "n_streams" (6), "discard" (1), "fwd_wave" (32), "one_stream",
+ * "cta_cap_a" / "cta_cap_b" (CTAs per SM of the two correlation passes,
+ * process-wide; defaults 0 = occupancy / 2, and 0 sets no cap),
  * "time_kernels" (1 = record a CUDA event pair on the context stream around
  * every launch; read back with tdg_kernel_time), "track_graphs" (default 1:
  * tdg_track / tdg_track_device batches that fit one correlation wave are
