@@ -937,10 +937,6 @@ CUtensorMap m_store_map(float2* M, int N1, int n_tiles, uint64_t Mstride, int n_
     return map;
 }
 
-// Waves of wave_pairs pairs; pass A of wave w on the context stream, pass B
-// on the second stream, M in a ring of `ring` wave buffers: B(w) waits for
-// A(w), A(w) waits for B(w - ring).  Pass B of wave w thus overlaps pass A of
-// wave w+1 and neither kernel's ramp or tail leaves SMs idle.
 // statistics (k_stats): one CTA per (slot, code) when there are enough of
 // them to fill the GPU, else each dot product split over several CTAs
 void launch_stats(tdg_ctx* ctx, const tdg::StatsDesc* sd, size_t n, uint32_t W, double fs, float threshold) {
@@ -969,6 +965,11 @@ void launch_stats(tdg_ctx* ctx, const tdg::StatsDesc* sd, size_t n, uint32_t W, 
     LAUNCHED();
 }
 
+// Waves of wave_pairs pairs; wave w's pass A on A-stream w % n_streams and its
+// pass B on B-stream w % n_streams, M in a ring of `ring` wave buffers: B(w)
+// waits for A(w), A(w) waits for B(w - ring).  Passes of neighbouring waves
+// thus overlap and no kernel's ramp or tail leaves SMs idle.  One wave
+// (small tracking batches) runs on the context stream without events.
 void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const std::vector<CorrJob>& jobs,
                       bool write_xc) {
     if (jobs.empty()) return;
