@@ -11,8 +11,15 @@ job), plus the real-time factor.
 
   value  device-timed, int16 stream already resident in HBM
          (tdg_demodulate_device + tdg_detect, detections left on device)
-  e2e    through the C-ABI tdg_search() from PINNED HOST int16 (H2D of the
-         stream and D2H of every Detection record inside the timed region)
+  e2e    the streaming C-ABI from PINNED HOST int16: tdg_ring_push of the
+         step's second into the device CircularBuffer + tdg_search_ring with
+         every Detection record copied back to pinned host memory (H2D and
+         D2H inside the timed region)
+
+Nothing is timed before a correctness gate passes (the reference's run_bench
+gate, proj/src/harness.cpp:58-73): the injected packets found at the right
+ToA, no absent code accepted, and window 0 x 9 bins x 32 codes equal to the
+reference's records (oracle/_ref) under the parity contract.
 
 Multi-GPU (torchrun): weak scaling by tag set -- rank r owns codes
 [64r, 64r+64) of the roster and searches the same stream; the per-step
@@ -55,17 +62,22 @@ def bytes_per_corr(n_bins, n_codes):
     return B_CODE_HALF / n_bins + B_REPLICA + B_WIN / n_codes
 
 
-def fp32_roof(achieved_tflops, clocks):
-    """The stage's real bound: FP32 issue.  Nominal FP32 peak = SMs x 128 lanes
-    x 2 flop (FMA) x the median SM clock measured during the timed region."""
-    import torch
-    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
-    mhz = (clocks or {}).get("sm_mhz") or 1965.0
-    peak = sms * 128 * 2 * mhz * 1e6 / 1e12
-    return {"achieved_tflops": achieved_tflops, "peak_tflops": peak, "frac": achieved_tflops / peak,
-            "peak_source": "nominal %d SMs x 128 FP32 lanes x 2 at the measured %.0f MHz median" % (sms, mhz),
-            "note": "SURVEY 8(d) 47.6 MFLOP/correlation (5 N log2 N convention) over the correlation stage; "
-                    "the stage is FP32-issue / latency bound, not HBM bound (DESIGN.md section 4)"}
+def roofline(n_units, stage_ms, fp32_peak_tflops, hbm_peak_gbs, bytes_corr, flop_corr=FLOP_CORR):
+    """SURVEY 8(d) roofline of the correlation stage: bound = FP32 (the
+    stage's arithmetic intensity sits at the FP32 ridge and the bin sweep
+    shares every code read), achieved = flops per correlation x correlations /
+    stage time, frac = achieved / peak; attainable corr/s = min(HBM peak /
+    bytes per corr, FP32 peak / flops per corr); the HBM fraction is kept as
+    a secondary figure."""
+    t = stage_ms / 1e3
+    achieved = n_units * flop_corr / t / 1e12
+    attainable = min(hbm_peak_gbs * 1e9 / bytes_corr, fp32_peak_tflops * 1e12 / flop_corr)
+    hbm = bytes_corr * n_units / t / 1e9
+    return {"bound": "fp32", "achieved": achieved, "peak": fp32_peak_tflops, "unit": "TFLOP/s",
+            "frac": achieved / fp32_peak_tflops, "attainable_corr_per_s": attainable,
+            "stage_corr_per_s": n_units / t, "frac_of_attainable": (n_units / t) / attainable,
+            "hbm": {"achieved": hbm, "peak": hbm_peak_gbs, "unit": "GB/s", "frac": hbm / hbm_peak_gbs,
+                    "algorithmic_bytes_per_corr": bytes_corr}}
 
 
 def peaks():
@@ -181,32 +193,80 @@ def make_inputs(rank, world, workload="search"):
     return bits_all[lo:min(roster, lo + per)], iq, inj, lo
 
 
+def cpu_model():
+    """CPU model, logical CPU count and max MHz from lscpu (the box's host)."""
+    info = {"model": None, "logical_cpus": os.cpu_count(), "max_mhz": None}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for l in out.splitlines():
+            k, _, v = l.partition(":")
+            v = v.strip()
+            if k.strip() == "Model name":
+                info["model"] = v
+            elif k.strip() in ("CPU max MHz", "CPU MHz") and info["max_mhz"] is None:
+                info["max_mhz"] = float(v)
+    except Exception:
+        pass
+    return info
+
+
+def reference_sample(bits, iq, n_codes, n_bins, threads, code_chunk=2):
+    """The reference's own searching loop (proj/src/recording.cpp:277-286: one
+    demodulate_window per (window, bin) shared by every code, then detect over
+    the codes) on window 0 of the stream, `n_bins` lo_freq bins x `n_codes`
+    codes, on `threads` host threads (oracle/_ref, tdref_search_bench_shared).
+    Returns (seconds, records [bin][code], stage thread-seconds)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refpy
+    from paper_2005_10445_b200._abi import demod_config
+    t, recs, st = refpy.search_bench_shared(iq[:2 * W], 0, demod_config(), BINS[:n_bins], bits[:n_codes], W, ADV, 1,
+                                            0.25, threads, code_chunk=code_chunk)
+    return t, recs.reshape(n_bins, n_codes), st
+
+
+def single_core_sample(bits, iq):
+    """One host core: 1 window x 1 bin x 8 codes through the same loop."""
+    t, _, st = reference_sample(bits, iq, 8, 1, 1, code_chunk=8)
+    return {"value": 8 / t, "unit": "corr/s", "cores": 1, "sample": "1 window x 1 bin x 8 codes (%.2f s)" % t,
+            "stage_s": st}
+
+
+def stage_split(st):
+    tot = sum(st.values()) or 1.0
+    return {k: round(v / tot, 4) for k, v in st.items()}
+
+
 def run_reference(args):
-    """Reference arm: oracle/_ref (the reference compiled in place) on the host."""
+    """Reference arm: oracle/_ref (the reference compiled in place) on the
+    host, like for like with the reference's own loop: one demodulation per
+    (window, bin) shared by all codes, detect() over the codes, work spread
+    over every host thread."""
     rank, _, world = dist_env()
     if rank != 0:
         return
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import refpy
-    from paper_2005_10445_b200._abi import demod_config
     if not refpy.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtagdsp_ref.so not built"}))
         return
-    cfg = demod_config()
     bits, iq, _, _ = make_inputs(0, 1)
     threads = os.cpu_count() or 1
     n_codes = args.ref_codes
-    # bounded sample: 1 window x all 9 bins x n_codes codes
-    times = []
+    times, stages = [], {"demod": 0.0, "correlation": 0.0, "peak_stats": 0.0}
     for i in range(args.warmup + args.steps):
-        t, dets = refpy.search_bench(iq, 0, cfg, BINS, bits[:n_codes], W, ADV, 1, 0.25, threads, code_chunk=1)
+        t, _, st = reference_sample(bits, iq, n_codes, len(BINS), threads)
         if i >= args.warmup:
             times.append(t)
+            for k in stages:
+                stages[k] += st[k]
     per_step = float(np.mean(times))
     units = 1 * len(BINS) * n_codes
     val = units / per_step
-    sample = "1 window x %d bins x %d codes (%d correlations) per step, %d host threads" % (
-        len(BINS), n_codes, units, threads)
+    single = single_core_sample(bits, iq)
+    cpu = cpu_model()
+    sample = ("1 window x %d bins x %d codes (%d correlations) per step: one demodulate_window per (window, bin) "
+              "shared by all codes, detect() over chunks of 2 codes, %d host threads" % (len(BINS), n_codes, units,
+                                                                                      threads))
     line = {
         "impl": "reference", "metric": "tag-code correlations/sec", "value": val, "unit": "corr/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
@@ -217,7 +277,8 @@ def run_reference(args):
         "paper_throughput_patterns": int(math.floor(val * (W / FS))),
         "paper_tags_searchable_50pct": int(math.floor(0.5 * val * (W / FS))),
         "cpu_baseline": {"value": val, "unit": "corr/s", "cores": threads, "kind": "reference", "sample": sample,
-                         "fft": "oracle/fftw_shim (no libfftw3f on the box)"},
+                         "fft": "oracle/fftw_shim (no libfftw3f on the box)", "cpu": cpu,
+                         "single_core": single, "stage_split": stage_split(stages)},
         "e2e": {"value": val, "unit": "corr/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -236,19 +297,50 @@ def workload_config(world, workload="search"):
                            world}
 
 
-def cpu_baseline_sample(bits, iq):
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import refpy
-    from paper_2005_10445_b200._abi import demod_config
-    if not refpy.available():
-        return None
-    threads = os.cpu_count() or 1
-    n_codes = 32
-    t, _ = refpy.search_bench(iq, 0, demod_config(), BINS, bits[:n_codes], W, ADV, 1, 0.25, threads, code_chunk=1)
-    units = len(BINS) * n_codes
-    return {"value": units / t, "unit": "corr/s", "cores": threads, "kind": "reference",
-            "sample": "1 window x %d bins x %d codes = %d correlations in %.1f s on %d host threads "
-                      "(FFT: oracle/fftw_shim, libfftw3f absent)" % (len(BINS), n_codes, units, t, threads)}
+def correctness_gate(recs, inj, code0, n_codes, ref_recs, bits, iq):
+    """Refuse to time a wrong pipeline (the reference's run_bench gate,
+    proj/src/harness.cpp:58-73): every injected packet of this rank's codes
+    that lies wholly inside a window is accepted at its nearest lo_freq bin
+    with |ToA error| < 0.5 sample, no absent code is accepted anywhere, and
+    the records of window 0 x all bins x the CPU sample's codes match the
+    reference's (oracle/_ref) under the parity contract (near-ties
+    documented with their margin on the reference's own xc).
+    recs: this rank's GPU records [window][bin][code]."""
+    problems, found = [], 0
+    mine = [(ci - code0, t, foff) for ci, t, _, foff in inj if code0 <= ci < code0 + n_codes]
+    for c, t, foff in mine:
+        a = t * FS
+        b = int(np.argmin(np.abs(BINS - foff)))
+        for wi in range(N_WIN):
+            s0 = wi * ADV
+            if s0 <= a and a + 65536 + 256 <= s0 + W:
+                r = recs[wi, b, c]
+                if not r["accepted"] or abs(float(r["toa_seconds"]) * FS - a) >= 0.5:
+                    problems.append(("injection", c + code0, wi, float(r["score"]), float(r["toa_seconds"]) * FS, a))
+                else:
+                    found += 1
+    injected = {c for c, _, _ in mine}
+    spurious = [(int(w), int(b), int(c)) for w, b, c in zip(*np.nonzero(recs["accepted"])) if int(c) not in injected]
+    problems += [("spurious",) + x for x in spurious]
+    report = None
+    if ref_recs is not None:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import refpy
+        from paritycheck import ParityReport, RefSlots
+        from paper_2005_10445_b200._abi import demod_config
+        nb, nc = ref_recs.shape
+        rs = RefSlots(refpy, demod_config(), bits, iq, W)
+        report = ParityReport("bench gate: window 0 x %d bins x %d codes" % (nb, nc))
+        for b in range(nb):
+            bad = rs.compare(recs[0, b, :nc], ref_recs[b], 0, BINS[b], FS, report=report)
+            problems += [("parity", b) + tuple(x) for x in bad]
+    gate = {"injections_found": found, "injections_expected": found + sum(p[0] == "injection" for p in problems),
+            "spurious": len(spurious), "ok": not problems}
+    if report is not None:
+        s = report.summary()
+        gate["parity"] = {k: s[k] for k in ("records", "peak_index_exact", "near_ties", "mismatches",
+                                             "max_delta_accepted_records")}
+    return gate, problems
 
 
 def run_tracking(args):
@@ -302,12 +394,44 @@ def run_tracking(args):
         res[str(B)] = {"tasks_per_s": B / float(np.mean(lat)), "p50_ms": float(np.percentile(lat, 50) * 1e3),
                        "p99_ms": float(np.percentile(lat, 99) * 1e3), "batches": int(lat.size),
                        "accepted_last_batch": int(out["accepted"].sum())}
+    # CPU beside it: the reference's tracking task body (demodulate_window +
+    # detect against one code prepared for the tracking shape,
+    # recording.cpp:360-378) on one host core -- the reference's scheduler is
+    # sequential -- over 32 tasks of the same pool, and the GPU's records of
+    # those tasks against the reference's (parity contract).
+    cpu, parity = None, None
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refpy
+    if refpy.available() and not args.no_cpu_baseline:
+        sel = pool[:32]
+        st = np.array([x[0] for x in sel], np.int64)
+        co = np.array([x[1] for x in sel], np.uint64)
+        t_cpu, want = refpy.track_bench(iq, 0, cfg, bits, TW, st, co, 0.25)
+        cpu = {"value": len(sel) / t_cpu, "unit": "tasks/s", "cores": 1, "kind": "reference",
+               "sample": "32 tracking tasks (16 injected packets + 16 misses), one at a time on one host core",
+               "cpu": cpu_model()}
+        got = np.zeros(len(sel), dtype=DETECTION_DTYPE)
+        tasks = np.zeros(len(sel), dtype=TRACK_TASK_DTYPE)
+        tasks["start"], tasks["code_index"] = st, co
+        capi._check(lib.tdg_track_device(ctx.handle, ctypes.byref(cfg), ctypes.c_void_p(iq_dev.data_ptr()), n, 0,
+                                         capi._ptr(tasks), len(sel), cs._h, 0.25, capi._ptr(got)))
+        from paritycheck import ParityReport, RefSlots
+        rep = ParityReport("tracking: 32 tasks")
+        bad = []
+        rs = RefSlots(refpy, cfg, bits, iq, TW)
+        for i in range(len(sel)):
+            bad += rs.compare(got[i:i + 1], want[i:i + 1], int(st[i]), cfg.lo_freq, FS, report=rep)
+        parity = {"records": rep.records, "peak_index_exact": rep.peak_exact, "near_ties": len(rep.near_ties),
+                  "mismatches": len(bad), "accepted": int(got["accepted"].sum())}
+        if bad:
+            sys.stderr.write(json.dumps({"error": "tracking parity failed", "bad": [str(b) for b in bad[:10]]}) + "\n")
+            sys.exit(3)
     line = {"metric": "tracking tasks/sec", "value": res["512"]["tasks_per_s"], "unit": "tasks/s", "n_gpus": 1,
             "higher_is_better": True, "dtype": "f32", "data": "synthetic (cfg2 scene; 16 injected packets tracked, "
             "other tasks are misses at random predicted times)",
             "config": {"workload": "cfg4: tracking windows W=96000 (2 ms pre + 10 ms post at 8 Ms/s), one code per "
                                    "task, batches of 1/8/64/512", "corr_len_b200": cs.info(0)["corr_len"]},
-            "batches": res}
+            "batches": res, "cpu_baseline": cpu, "parity": parity}
     print(json.dumps(line))
 
 
@@ -320,7 +444,7 @@ def main():
     ap.add_argument("--workload", default="search", choices=["search", "roster", "streams", "tracking"],
                     help="search: BASELINE configs[1] (the headline line); roster: configs[2]; "
                          "tracking: configs[3]; streams: configs[4]")
-    ap.add_argument("--ref-codes", type=int, default=16)
+    ap.add_argument("--ref-codes", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-step", action="store_true",
                     help="run one extra device step between cudaProfilerStart/Stop (ncu --profile-from-start off)")
@@ -373,7 +497,7 @@ def main():
     def step_device():
         capi._check(lib.tdg_demodulate_device(ctx.handle, win._h, ctypes.byref(cfg), capi._ptr(bins), bins.size,
                                               ctypes.c_void_p(iq_dev.data_ptr()), n_complex, 0, ADV, N_WIN))
-        capi._check(lib.tdg_detect(ctx.handle, win._h, cs._h, 0.25, FS, None))
+        capi._check(lib.tdg_detect(ctx.handle, win._h, cs._h, 0.25, FS, None, 0))
 
     nout = ctypes.c_uint64()
 
@@ -412,6 +536,27 @@ def main():
         t = torch.tensor([x], dtype=torch.float64, device=coll_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+    # ---- correctness gate: nothing is timed unless the pipeline is right ----
+    gate_recs = capi.search(ctx, cfg, bins, iq, cs, W, ADV).reshape(N_WIN, len(BINS), n_codes)
+    cpu, ref_recs = None, None
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refpy
+    if rank == 0 and not args.no_cpu_baseline and refpy.available():
+        threads = os.cpu_count() or 1
+        nref = min(32, n_codes)
+        t_ref, ref_recs, st = reference_sample(bits, iq, nref, len(BINS), threads)
+        cpu = {"value": len(BINS) * nref / t_ref, "unit": "corr/s", "cores": threads, "kind": "reference",
+               "sample": "1 window x %d bins x %d codes = %d correlations in %.2f s on %d host threads: one "
+                         "demodulate_window per (window, bin) shared by all codes, detect() over chunks of 2 codes "
+                         "(FFT: oracle/fftw_shim, libfftw3f absent)" % (len(BINS), nref, len(BINS) * nref, t_ref,
+                                                                         threads),
+               "cpu": cpu_model(), "stage_split": stage_split(st)}
+    gate, problems = correctness_gate(gate_recs, inj, code0, n_codes, ref_recs, bits, iq)
+    if problems:
+        sys.stderr.write(json.dumps({"error": "correctness gate failed; not timing", "gate": gate,
+                                     "problems": [list(map(str, p)) for p in problems[:20]]}) + "\n")
+        sys.exit(3)
 
     # ---- device-resident timed region ---------------------------------------
     clk = Clocks(local).start()
@@ -465,12 +610,21 @@ def main():
     ctx.set_option("time_kernels", 0)
 
     # ---- roofline of the dominant stage: the correlation engine -------------
-    # (k_corr_pass pass A + pass B on overlapped streams, one per-step event pair)
+    # (k_corr_pass pass A + pass B on overlapped streams, one per-step event
+    # pair).  SURVEY 8(d): the stage is FP32 bound (AI ~12.7 flop/B at the
+    # ridge, and the 9-bin sweep shares each code read 9 ways), so the bound
+    # is FP32: achieved = 47.6 MFLOP per correlation x correlations per step /
+    # stage time; peak = the packed-FFMA2 rate MEASURED on this GPU now
+    # (tdg_fp32_peak, the instruction the codelets use); attainable corr/s =
+    # min(HBM peak / bytes per corr, FP32 peak / flops per corr).
     pk = peaks()
     n_corr_launch, ms_corr = kt["corr"]
     corr_ms_step = ms_corr / max(1, n_corr_launch)
     bpc = bytes_per_corr(len(BINS), n_codes)
-    achieved = bpc * n_units / (corr_ms_step / 1e3) / 1e9
+    hbm_achieved = bpc * n_units / (corr_ms_step / 1e3) / 1e9
+    ffma_peak, ffma2_peak = capi.fp32_peak(local)
+    fp32_peak = max(ffma_peak, ffma2_peak)
+    roof = roofline(n_units, corr_ms_step, fp32_peak, pk["hbm_gbs"], bpc)
     total_ms = sum(v[1] for v in kt.values())
     shares = {k: round(v[1] / total_ms, 4) if total_ms else None for k, v in kt.items()}
     traffic = None
@@ -483,7 +637,6 @@ def main():
 
     if rank != 0:
         return
-    cpu = None if args.no_cpu_baseline else cpu_baseline_sample(bits, iq)
     clocks = clk.summary()
     line = {
         "metric": "tag-code correlations/sec", "value": value, "unit": "corr/s", "n_gpus": world,
@@ -492,6 +645,7 @@ def main():
         "data": "synthetic (numpy scene: 16 of the codes injected at known fractional delays, offsets "
                 "U(-200,200) kHz, SNR {0,5,10,20} dB in 10 dB noise; int16 at scale 8192)",
         "config": dict(workload_config(world, args.workload), corr_len_b200=corr_len_used),
+        "gate": gate,
         # stream seconds searched per wall second for the whole roster (64 x
         # n_gpus codes) x 9 bins: N_WIN windows x advance per step
         "real_time_factor": (N_WIN * ADV / FS) / (ms_max / 1e3),
@@ -511,18 +665,17 @@ def main():
                         "stream) + tdg_search_ring (Detection records -> pinned host), upload of step k+1 "
                         "overlapping the search of step k"},
         "gpu_launches": int(launches),
-        "roofline": {"bound": "hbm",
-                     "kernel": "correlation engine per step: k_corr_pass<27,32,32,32,0> (spectral product + "
-                               "first inverse-FFT pass) and k_corr_pass<...,1> (second pass + argmax), "
-                               "%d launches in waves of %d pairs over 6 pass-A + 6 pass-B streams" % (
-                                   2 * (((n_codes + 1) // 2 * N_WIN * len(BINS) + WAVE_PAIRS - 1) // WAVE_PAIRS),
-                                   WAVE_PAIRS),
-                     "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
-                     "traffic": traffic, "peak_source": pk["source"],
-                     "traffic_note": "dram__bytes_read+write of all correlation launches of one step, warm L2 "
-                                     "(ncu --cache-control none, profiles/traffic.json)",
-                     "algorithmic_bytes_per_corr": bpc, "corr_per_step": n_units, "stage_ms_per_step": corr_ms_step,
-                     "fp32": fp32_roof(n_units * FLOP_CORR / (corr_ms_step / 1e3) / 1e12, clocks)},
+        "roofline": dict(roof, **{
+            "kernel": "correlation engine per step: k_corr_pass<27,32,32,32,0> (spectral product + first "
+                      "inverse-FFT pass) and k_corr_pass<...,1> (second pass + argmax) in waves over 6 pass-A + 6 "
+                      "pass-B streams",
+            "traffic": traffic,
+            "peak_source": "measured live on this GPU (tdg_fp32_peak): packed FFMA2 %.1f TFLOP/s, scalar FFMA "
+                           "%.1f TFLOP/s; peak = the larger" % (ffma2_peak, ffma_peak),
+            "flops_per_corr": FLOP_CORR, "corr_per_step": n_units, "stage_ms_per_step": corr_ms_step,
+            "traffic_note": "dram__bytes_read+write of all correlation launches of one step (profiles/traffic.json, "
+                            "ncu); algorithmic %.4g B/step" % (bpc * n_units),
+            "hbm_peak_source": pk["source"]}),
         "kernel_ms_per_step": {k: v[1] / args.steps for k, v in kt.items()},
         "kernel_share": shares,
         "clocks": clocks,

@@ -114,9 +114,19 @@ int tdg_windows_get_du(tdg_ctx* ctx, const tdg_windows* w, uint64_t slot, float*
  * FFT + |xc| first-index argmax (the xc vector never reaches HBM), then
  * parabolic refinement, (w_c, q, p_c) statistics, score, ToA and accept.
  * out receives n_slots*n_codes records ordered [slot][code] (slot = window *
- * n_bins + bin) in HOST memory.  toa uses each slot's window_start. */
+ * n_bins + bin) in HOST memory (out_cap >= n_slots*n_codes, else TDG_EINVAL;
+ * out may be NULL: records stay on the device).  toa uses each slot's
+ * window_start. */
 int tdg_detect(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float threshold,
-               double sample_rate, tdg_detection* out);
+               double sample_rate, tdg_detection* out, uint64_t out_cap);
+/* detect() over a subset of the code set -- the reference's
+ * span<const TransformedCode* const> (detector.hpp:103-106): records
+ * [slot][k] for code idx[k] (repeats allowed); only the stored code pairs the
+ * subset touches are correlated.  out may be NULL (records stay on the
+ * device); else out_cap >= n_slots*n_idx. */
+int tdg_detect_codes(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const int64_t* idx,
+                     uint64_t n_idx, float threshold, double sample_rate, tdg_detection* out,
+                     uint64_t out_cap);
 /* batch_xcorr (proj/src/detector.cpp:102-120) for one slot: the full xc
  * (lags [0, W)) of each requested code, normalised like the reference
  * inverse (1/N), into HOST out (n_idx x W).  Test/diagnostic path. */
@@ -177,8 +187,8 @@ int tdg_track_ring(tdg_ctx* ctx, tdg_ring* ring, const tdg_demod_config* cfg, co
 
 /* Tuning / profiling knobs (0 = default): "wave_pairs" (8), "ring" (3),
  * "n_streams" (6), "discard" (1), "fwd_wave" (32), "one_stream",
- * "cta_cap_a" / "cta_cap_b" (CTAs per SM of the two correlation passes,
- * process-wide; defaults 0 = occupancy / 2, and 0 sets no cap),
+ * "cta_cap_a" / "cta_cap_b" (CTAs per SM of the two correlation passes of
+ * this context; defaults 0 = occupancy / 2, and 0 sets no cap),
  * "time_kernels" (1 = record a CUDA event pair on the context stream around
  * every launch; read back with tdg_kernel_time), "track_graphs" (default 1:
  * tdg_track / tdg_track_device batches that fit one correlation wave are
@@ -191,6 +201,9 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value);
  * "stats".  Synchronises the context stream. */
 int tdg_kernel_time(tdg_ctx* ctx, const char* name, uint64_t* count, double* total_ms);
 int tdg_kernel_time_reset(tdg_ctx* ctx);
+/* FP32 issue-rate probe (bench.py's roofline denominator): TFLOP/s of scalar
+ * FFMA and of packed FFMA2 on `device` at its current clock. */
+int tdg_fp32_peak(int device, double* ffma_tflops, double* ffma2_tflops);
 
 #ifdef __cplusplus
 }

@@ -290,7 +290,7 @@ inline std::vector<Detection> detect(std::span<const float> d, std::span<const f
     tdg_windows* w = cache.window(W);
     detail::check(tdg_windows_set_du(cache.handle(), w, 0, d.data(), u.data(), cfg.window_start));
     std::vector<tdg_detection> all(tdg_codeset_size(set));
-    detail::check(tdg_detect(cache.handle(), w, set, cfg.threshold, sample_rate, all.data()));
+    detail::check(tdg_detect(cache.handle(), w, set, cfg.threshold, sample_rate, all.data(), all.size()));
     out.reserve(codes.size());
     for (auto* tc : codes) out.push_back(detail::to_detection(all[tc->index], tc->tag_id));
     (void)timings;

@@ -442,4 +442,162 @@ double tdref_search_bench(const int16_t* iq, uint64_t n_complex, int64_t stream_
     return rc ? -double(rc) : elapsed;
 }
 
+// CPU reference arm, like for like with the reference's own loop
+// (proj/src/recording.cpp:277-286): ONE demodulate_window per (window, bin),
+// shared by every code, then detect() over the codes.  Spread over `threads`
+// host threads in two phases: (1) the (window, bin) demodulations, (2)
+// detect() over (window, bin, chunk of code_chunk codes) tasks, each thread
+// with its own PlanCache (fft.hpp:13-16).  Codes are prepared before timing,
+// split over the threads (each TransformedCode is read-only afterwards).
+// stage_s (optional, 3 doubles) receives summed thread-seconds of
+// demodulation, correlation and peak+statistics (DetectTimings,
+// detector.hpp:95-98; the split of harness.hpp:7-11).  Returns the wall time
+// of the two phases in seconds (<0 on error); detections [window][bin][code].
+double tdref_search_bench_shared(const int16_t* iq, uint64_t n_complex, int64_t stream_start,
+                                 const tdg_demod_config* cfg, const double* lo_bins, uint64_t n_bins,
+                                 const uint8_t* bits, uint64_t n_codes, uint64_t window_len,
+                                 uint64_t advance, uint64_t n_windows, float threshold, int threads,
+                                 int code_chunk, tdg_detection* out, double* stage_s) {
+    double elapsed = -1.0;
+    int rc = guard([&] {
+        if (threads < 1) threads = 1;
+        if (code_chunk < 1) code_chunk = int(n_codes);
+        if (n_windows && (n_windows - 1) * advance + window_len > n_complex)
+            throw std::invalid_argument("search_bench: windows exceed the stream");
+        const DemodConfig base = to_cfg(*cfg);
+        const uint64_t nbits = cfg->mod.packet_bits;
+        struct Ctx {
+            PlanCache cache;
+            CodeCache codes;
+            double demod_s = 0, corr_s = 0, peak_s = 0;
+        };
+        std::vector<std::unique_ptr<Ctx>> ctx(static_cast<size_t>(threads));
+        for (auto& c : ctx) c = std::make_unique<Ctx>();
+        std::vector<const TransformedCode*> tcs(n_codes, nullptr);
+        std::vector<std::string> errs(static_cast<size_t>(threads));
+        auto run = [&](auto&& body) {
+            std::vector<std::thread> pool;
+            for (int t = 0; t < threads; ++t)
+                pool.emplace_back([&, t] {
+                    try {
+                        body(t);
+                    } catch (const std::exception& e) {
+                        errs[size_t(t)] = e.what();
+                    }
+                });
+            for (auto& th : pool) th.join();
+            for (auto& e : errs)
+                if (!e.empty()) throw std::runtime_error(e);
+        };
+        run([&](int t) {   // untimed: prepare_code (detect_recording :271-274), codes split over threads
+            WindowShape shape{size_t(window_len), base};
+            for (uint64_t c = uint64_t(t); c < n_codes; c += uint64_t(threads)) {
+                TagCode code;
+                code.tag_id = "t" + std::to_string(c);
+                code.mod = base.mod;
+                code.bits.assign(bits + c * nbits, bits + (c + 1) * nbits);
+                tcs[c] = &prepare_code(code, shape, ctx[size_t(t)]->cache, ctx[size_t(t)]->codes);
+            }
+        });
+        const uint64_t n_slots = n_windows * n_bins;
+        std::vector<DemodResult> demod(n_slots);
+        const uint64_t chunks = (n_codes + uint64_t(code_chunk) - 1) / uint64_t(code_chunk);
+        std::atomic<uint64_t> next{0};
+        const auto t0 = std::chrono::steady_clock::now();
+        run([&](int t) {   // phase 1: one demodulation per (window, bin)
+            Ctx& c = *ctx[size_t(t)];
+            for (;;) {
+                const uint64_t slot = next.fetch_add(1);
+                if (slot >= n_slots) break;
+                const uint64_t w = slot / n_bins, b = slot % n_bins, start = w * advance;
+                const auto a = std::chrono::steady_clock::now();
+                RawSampleBlock blk;
+                blk.sample_rate = base.mod.sample_rate;
+                blk.start_time = stream_start + int64_t(start);
+                blk.samples.assign(iq + 2 * start, iq + 2 * (start + window_len));
+                DemodConfig dcfg = base;
+                dcfg.lo_freq = lo_bins[b];
+                demod[slot] = demodulate_window(blk, dcfg, c.cache);
+                c.demod_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
+            }
+        });
+        next = 0;
+        run([&](int t) {   // phase 2: detect over code chunks of every slot
+            Ctx& c = *ctx[size_t(t)];
+            for (;;) {
+                const uint64_t task = next.fetch_add(1);
+                if (task >= n_slots * chunks) break;
+                const uint64_t slot = task / chunks, ch = task % chunks;
+                const uint64_t w = slot / n_bins, b = slot % n_bins;
+                const int64_t ws = stream_start + int64_t(w * advance);
+                const uint64_t c0 = ch * uint64_t(code_chunk), c1 = std::min(n_codes, c0 + uint64_t(code_chunk));
+                std::span<const TransformedCode* const> sub(tcs.data() + c0, c1 - c0);
+                DetectTimings tm;
+                auto dets = detect(demod[slot].d, demod[slot].u, sub, DetectionConfig{threshold, ws},
+                                   base.mod.sample_rate, c.cache, &tm);
+                c.corr_s += tm.correlation_s;
+                c.peak_s += tm.peak_stats_s;
+                for (uint64_t k = 0; k < dets.size(); ++k)
+                    fill_detection(dets[k], int32_t(c0 + k), int32_t(b), ws, out + slot * n_codes + c0 + k);
+            }
+        });
+        elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (stage_s) {
+            stage_s[0] = stage_s[1] = stage_s[2] = 0.0;
+            for (auto& c : ctx) {
+                stage_s[0] += c->demod_s;
+                stage_s[1] += c->corr_s;
+                stage_s[2] += c->peak_s;
+            }
+        }
+    });
+    return rc ? -double(rc) : elapsed;
+}
+
+// Tracking tasks on the CPU (the Tracking branch of simulate_recording,
+// proj/src/recording.cpp:360-378): per task demodulate_window of
+// [start, start + window_len) at cfg->lo_freq, then detect() against its one
+// code prepared for the tracking shape.  Single thread (the reference's
+// scheduler is sequential, scheduler.hpp:90-92).  Returns seconds of the
+// timed loop (<0 on error); out[i] = task i's Detection.
+double tdref_track_bench(const int16_t* iq, uint64_t n_complex, int64_t stream_start, const tdg_demod_config* cfg,
+                         const uint8_t* bits, uint64_t n_codes, uint64_t window_len, const int64_t* starts,
+                         const uint64_t* code_idx, uint64_t n_tasks, float threshold, tdg_detection* out) {
+    double elapsed = -1.0;
+    int rc = guard([&] {
+        const DemodConfig base = to_cfg(*cfg);
+        const uint64_t nbits = cfg->mod.packet_bits;
+        PlanCache cache;
+        CodeCache codes;
+        std::vector<const TransformedCode*> tcs(n_codes);
+        WindowShape shape{size_t(window_len), base};
+        for (uint64_t c = 0; c < n_codes; ++c) {
+            TagCode code;
+            code.tag_id = "t" + std::to_string(c);
+            code.mod = base.mod;
+            code.bits.assign(bits + c * nbits, bits + (c + 1) * nbits);
+            tcs[c] = &prepare_code(code, shape, cache, codes);
+        }
+        const auto t0 = std::chrono::steady_clock::now();
+        for (uint64_t i = 0; i < n_tasks; ++i) {
+            const int64_t s0 = starts[i];
+            if (s0 < stream_start || uint64_t(s0 - stream_start) + window_len > n_complex)
+                throw std::invalid_argument("track_bench: task window outside the block");
+            if (code_idx[i] >= n_codes) throw std::invalid_argument("track_bench: code index");
+            RawSampleBlock blk;
+            blk.sample_rate = base.mod.sample_rate;
+            blk.start_time = s0;
+            const uint64_t off = uint64_t(s0 - stream_start);
+            blk.samples.assign(iq + 2 * off, iq + 2 * (off + window_len));
+            auto demod = demodulate_window(blk, base, cache);
+            const TransformedCode* one[1] = {tcs[code_idx[i]]};
+            auto dets = detect(demod.d, demod.u, std::span<const TransformedCode* const>(one, 1),
+                               DetectionConfig{threshold, s0}, base.mod.sample_rate, cache);
+            fill_detection(dets[0], int32_t(code_idx[i]), 0, s0, out + i);
+        }
+        elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    });
+    return rc ? -double(rc) : elapsed;
+}
+
 }  // extern "C"

@@ -63,6 +63,11 @@ def lib():
             "tdref_search_bench": (ctypes.c_double, [_P, _U64, _I64, ctypes.POINTER(DemodConfig), _P, _U64, _P,
                                                      _U64, _U64, _U64, _U64, ctypes.c_float, ctypes.c_int,
                                                      ctypes.c_int, _P]),
+            "tdref_search_bench_shared": (ctypes.c_double, [_P, _U64, _I64, ctypes.POINTER(DemodConfig), _P, _U64,
+                                                            _P, _U64, _U64, _U64, _U64, ctypes.c_float, ctypes.c_int,
+                                                            ctypes.c_int, _P, _P]),
+            "tdref_track_bench": (ctypes.c_double, [_P, _U64, _I64, ctypes.POINTER(DemodConfig), _P, _U64, _U64, _P,
+                                                    _P, _U64, ctypes.c_float, _P]),
         }
         for k, (r, a) in sig.items():
             f = getattr(L, k)
@@ -264,6 +269,40 @@ def search_bench(iq, stream_start, cfg, lo_bins, bits, window_len, advance, n_wi
     t = lib().tdref_search_bench(_p(iq), iq.size // 2, stream_start, ctypes.byref(cfg), _p(bins), bins.size,
                                  _p(bits), n_codes, window_len, advance, n_windows, threshold, threads, code_chunk,
                                  _p(out))
+    if t < 0:
+        _ck(int(-t))
+    return t, out
+
+
+def search_bench_shared(iq, stream_start, cfg, lo_bins, bits, window_len, advance, n_windows, threshold, threads,
+                        code_chunk=4):
+    """The reference's own loop (one demodulate_window per (window, bin),
+    shared by all codes) on `threads` host threads.  Returns (seconds,
+    detections [w][b][c], stage thread-seconds {demod, correlation,
+    peak_stats})."""
+    iq = np.ascontiguousarray(iq, dtype=np.int16)
+    bins = np.ascontiguousarray(lo_bins, dtype=np.float64)
+    bits = np.ascontiguousarray(np.atleast_2d(bits), dtype=np.uint8)
+    n_codes = bits.shape[0]
+    out = np.zeros(n_windows * bins.size * n_codes, DETECTION_DTYPE)
+    st = np.zeros(3, np.float64)
+    t = lib().tdref_search_bench_shared(_p(iq), iq.size // 2, stream_start, ctypes.byref(cfg), _p(bins), bins.size,
+                                        _p(bits), n_codes, window_len, advance, n_windows, threshold, threads,
+                                        code_chunk, _p(out), _p(st))
+    if t < 0:
+        _ck(int(-t))
+    return t, out, {"demod": float(st[0]), "correlation": float(st[1]), "peak_stats": float(st[2])}
+
+
+def track_bench(iq, stream_start, cfg, bits, window_len, starts, code_idx, threshold):
+    """Tracking tasks through the reference (single thread): (seconds, detections)."""
+    iq = np.ascontiguousarray(iq, dtype=np.int16)
+    bits = np.ascontiguousarray(np.atleast_2d(bits), dtype=np.uint8)
+    st = np.ascontiguousarray(starts, dtype=np.int64)
+    ci = np.ascontiguousarray(code_idx, dtype=np.uint64)
+    out = np.zeros(st.size, DETECTION_DTYPE)
+    t = lib().tdref_track_bench(_p(iq), iq.size // 2, stream_start, ctypes.byref(cfg), _p(bits), bits.shape[0],
+                                window_len, _p(st), _p(ci), st.size, threshold, _p(out))
     if t < 0:
         _ck(int(-t))
     return t, out

@@ -12,7 +12,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtagdsp_gpu.so")
 SOURCES = ["tagdsp_gpu.cu"]
-DEPS = SOURCES + ["kernels.cuh", "codelets.cuh", "corr_v3.cuh", "tma.cuh"]
+DEPS = SOURCES + ["kernels.cuh", "codelets.cuh", "corr_v3.cuh", "tma.cuh", "peak.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 

@@ -71,7 +71,8 @@ _PROTOS = {
                                              _U64]),
     "tdg_windows_set_du": (ctypes.c_int, [_P, _P, _U64, _P, _P, _I64]),
     "tdg_windows_get_du": (ctypes.c_int, [_P, _P, _U64, _P, _P]),
-    "tdg_detect": (ctypes.c_int, [_P, _P, _P, ctypes.c_float, ctypes.c_double, _P]),
+    "tdg_detect": (ctypes.c_int, [_P, _P, _P, ctypes.c_float, ctypes.c_double, _P, _U64]),
+    "tdg_detect_codes": (ctypes.c_int, [_P, _P, _P, _P, _U64, ctypes.c_float, ctypes.c_double, _P, _U64]),
     "tdg_batch_xcorr": (ctypes.c_int, [_P, _P, _U64, _P, _P, _U64, _P]),
     "tdg_search": (ctypes.c_int, [_P, ctypes.POINTER(DemodConfig), _P, _U64, _P, _U64, _I64, _U64, _U64, _P,
                                   ctypes.c_float, _P, _U64, ctypes.POINTER(_U64)]),
@@ -91,6 +92,7 @@ _PROTOS = {
     "tdg_set_option": (ctypes.c_int, [_P, ctypes.c_char_p, _I64]),
     "tdg_kernel_time": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.POINTER(_U64), ctypes.POINTER(ctypes.c_double)]),
     "tdg_kernel_time_reset": (ctypes.c_int, [_P]),
+    "tdg_fp32_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
 }
 EXPORTED_SYMBOLS = sorted(_PROTOS)
 
@@ -125,6 +127,13 @@ def _ptr(a):
 
 def kernel_launches():
     return int(lib().tdg_kernel_launches())
+
+
+def fp32_peak(device=0):
+    """(FFMA, FFMA2) TFLOP/s measured on `device` at its current clock."""
+    a, b = ctypes.c_double(), ctypes.c_double()
+    _check(lib().tdg_fp32_peak(int(device), ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
 
 
 def pad_length(n):
@@ -320,10 +329,18 @@ def demodulate_window(ctx, iq, start, cfg):
         w.close()
 
 
-def detect(ctx, windows, codes, threshold=0.25, sample_rate=8.0e6):
-    """detect() for every slot x code -> DETECTION_DTYPE records [slot][code]."""
-    out = np.zeros(windows.slots * len(codes), dtype=DETECTION_DTYPE)
-    _check(lib().tdg_detect(ctx.handle, windows._h, codes._h, float(threshold), float(sample_rate), _ptr(out)))
+def detect(ctx, windows, codes, threshold=0.25, sample_rate=8.0e6, idx=None):
+    """detect() for every slot x code (or the codes `idx`, in that order)
+    -> DETECTION_DTYPE records [slot][code]."""
+    if idx is None:
+        out = np.zeros(windows.slots * len(codes), dtype=DETECTION_DTYPE)
+        _check(lib().tdg_detect(ctx.handle, windows._h, codes._h, float(threshold), float(sample_rate), _ptr(out),
+                                out.size))
+        return out
+    idx = np.ascontiguousarray(np.atleast_1d(idx), dtype=np.int64)
+    out = np.zeros(windows.slots * idx.size, dtype=DETECTION_DTYPE)
+    _check(lib().tdg_detect_codes(ctx.handle, windows._h, codes._h, _ptr(idx), idx.size, float(threshold),
+                                  float(sample_rate), _ptr(out), out.size))
     return out
 
 

@@ -22,6 +22,7 @@
 #include "tagdsp_gpu.h"
 #include "kernels.cuh"
 #include "corr_v3.cuh"
+#include "peak.cuh"
 #include <cudaTypedefs.h>
 
 namespace {
@@ -343,15 +344,20 @@ void launch_fwd2(int L, bool split, dim3 grid, cudaStream_t st, const tdg::SeqPa
     fail(TDG_ERANGE, "fwd2: length %d", L);
 }
 
-int g_num_sms = 0;
-
+// SM count of the current device (cached per device: one process may drive
+// several GPUs, one context each)
 int num_sms() {
-    if (!g_num_sms) {
-        int dev = 0;
-        CK(cudaGetDevice(&dev));
-        CK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-    }
-    return g_num_sms;
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int n = 0;
+    CK(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    cache[dev] = n;
+    return n;
 }
 
 template <class K>
@@ -379,13 +385,9 @@ int persistent_grid(K* kernel, int threads, size_t smem, int n_items) {
     return std::max(1, std::min(n_items, per_sm * num_sms()));
 }
 
-// max CTAs per SM of pass A / pass B (0 = occupancy).  Pass B at 2 of its 3
-// leaves SM room for the next waves' pass A on the other streams (A/B: +0.8 %
-// device and e2e, burst and sustained)
-int g_cta_cap[2] = {0, 2};
-
+// cap: max CTAs per SM of the pass (0 = occupancy; per context, tdg_ctx::cta_cap)
 template <int TYPE>
-void launch_pass(int N1, int N2, cudaStream_t st, const tdg::CorrSched& S) {
+void launch_pass(int N1, int N2, cudaStream_t st, const tdg::CorrSched& S, int cap) {
     const int n_items = TYPE == 0 ? S.nA : S.nB;
 #define X(L1, P1, Q1, L2, P2, Q2)                                                       \
     if (N1 == L1 && N2 == L2) {                                                         \
@@ -395,7 +397,7 @@ void launch_pass(int N1, int N2, cudaStream_t st, const tdg::CorrSched& S) {
         const size_t sm = F::SMEM + ((TYPE == 0 ? S.ngw * sizeof(tdg::CorrGroup<tdg::kGroup>)       \
                                                 : S.wave_pairs * sizeof(tdg::CorrPairOut)) + 15) / 16 * 16; \
         int grid = persistent_grid(k, F::NT, sm, n_items);                              \
-        if (g_cta_cap[TYPE] > 0) grid = std::min(grid, g_cta_cap[TYPE] * num_sms());   \
+        if (cap > 0) grid = std::min(grid, cap * num_sms());                            \
         if (STREAM_OPS) k<<<grid, F::NT, sm, st>>>(S);                                  \
         LAUNCHED();                                                                     \
         return;                                                                         \
@@ -509,10 +511,7 @@ struct tdg_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
     std::map<int, std::unique_ptr<DevBuf>> tw;   // per pass length: w_L^{+a c}, index a*Q + c
-    // filter spectra cache
-    std::vector<double> hkey;   // filter_spectra cache key
-    DevBuf hspec;
-    int clen = 0;
+    int clen = 0;               // composed filter length of the last filter_spectra key
     // scratch
     DevBuf T, M, keys, det_dev, stream_buf, stats_part, stats_ctr;
     // streams + events of the multi-stream correlation pipeline
@@ -558,6 +557,10 @@ struct tdg_ctx {
     int64_t discard = 1;         // drop consumed M tiles from L2
     int64_t one_stream = 0;      // tuning: run pass B on the context stream too (no overlap)
     int64_t fwd_wave = 32;       // sequence pairs per forward-FFT wave
+    // max CTAs per SM of pass A / pass B (0 = occupancy).  Pass B at 2 of its 3
+    // leaves SM room for the next waves' pass A on the other streams (A/B: +0.8 %
+    // device and e2e, burst and sustained)
+    int cta_cap[2] = {0, 2};
     // optional per-launch CUDA-event timing (bench.py roofline)
     bool time_kernels = false;
     struct KTime {
@@ -606,7 +609,8 @@ struct tdg_ctx {
             }
         auto buf = std::make_unique<DevBuf>();
         buf->ensure(h.size() * sizeof(float2));
-        CK(cudaMemcpy(buf->p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(buf->p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice, stream));
+        CK(cudaStreamSynchronize(stream));
         const float2* p = buf->as<float2>();
         tw[L] = std::move(buf);
         return p;
@@ -635,7 +639,8 @@ struct tdg_ctx {
             }
         auto buf = std::make_unique<DevBuf>();
         buf->ensure(h.size() * sizeof(float2));
-        CK(cudaMemcpy(buf->p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(buf->p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice, stream));
+        CK(cudaStreamSynchronize(stream));
         const float2* p = buf->as<float2>();
         twf[key] = std::move(buf);
         return p;
@@ -658,7 +663,8 @@ struct tdg_ctx {
             }
         auto buf = std::make_unique<DevBuf>();
         buf->ensure(h.size() * sizeof(float2));
-        CK(cudaMemcpy(buf->p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(buf->p, h.data(), h.size() * sizeof(float2), cudaMemcpyHostToDevice, stream));
+        CK(cudaStreamSynchronize(stream));
         const float2* p = buf->as<float2>();
         twi[key] = std::move(buf);
         return p;
@@ -673,7 +679,19 @@ struct tdg_ctx {
         return pk.at<T>(off);
     }
 
-    // FFT_1024 spectra of the LO-shifted composed filters for a bin set.
+    // FFT_1024 spectra of the LO-shifted composed filters for a bin set.  One
+    // device buffer per key (configuration + bins), kept in a small LRU: a
+    // buffer is never rewritten while kernels queued on the context stream
+    // (or captured in a tracking graph) may still read it.  Eviction frees
+    // the buffer (cudaFree waits for the device) and drops captured graphs.
+    struct HSpec {
+        std::vector<double> key;
+        DevBuf buf;
+        int clen = 0;
+        uint64_t last_use = 0;
+    };
+    std::vector<std::unique_ptr<HSpec>> hspecs;
+    uint64_t hspec_clock = 0;
     const float2* filter_spectra(const tdg_demod_config& c, const std::vector<double>& bins) {
         validate_cfg(c);
         // cache key: the parameters the composed filters depend on, then the bins
@@ -681,7 +699,12 @@ struct tdg_ctx {
                               c.mod.freq_zero,       double(c.mod.packet_bits),
                               c.bandpass_center,     c.bandpass_width, double(c.bandpass_taps)};
         k.insert(k.end(), bins.begin(), bins.end());
-        if (k == hkey) return hspec.as<float2>();
+        for (auto& h : hspecs)
+            if (h->key == k) {
+                h->last_use = ++hspec_clock;
+                clen = h->clen;
+                return h->buf.as<float2>();
+            }
         const size_t spb = samples_per_bit(c.mod);
         std::vector<cfloat> hbp, hm;
         fill_bandpass(c.bandpass_center, c.bandpass_width, size_t(c.bandpass_taps), c.mod.sample_rate, hbp);
@@ -689,12 +712,12 @@ struct tdg_ctx {
         const auto h1c = convolve(hbp, hm);
         fill_matched(c.mod.freq_zero, spb, c.mod.sample_rate, hm);
         const auto h0c = convolve(hbp, hm);
-        clen = int(h1c.size());
-        if (clen > 1024 - 32) fail(TDG_ERANGE, "composed filter of %d taps exceeds the 1024-point demod block", clen);
+        const int cl = int(h1c.size());
+        if (cl > 1024 - 32) fail(TDG_ERANGE, "composed filter of %d taps exceeds the 1024-point demod block", cl);
         const double pi = 3.14159265358979323846;
         std::vector<float2> H(bins.size() * 2 * 1024);
         std::vector<std::complex<double>> tw(1024);
-        for (int k = 0; k < 1024; ++k) tw[size_t(k)] = std::polar(1.0, -2.0 * pi * k / 1024.0);
+        for (int kk = 0; kk < 1024; ++kk) tw[size_t(kk)] = std::polar(1.0, -2.0 * pi * kk / 1024.0);
         for (size_t b = 0; b < bins.size(); ++b) {
             const double om = 2.0 * pi * bins[b] / c.mod.sample_rate;
             for (int f = 0; f < 2; ++f) {
@@ -709,10 +732,24 @@ struct tdg_ctx {
                 }
             }
         }
-        hspec.ensure(H.size() * sizeof(float2));
-        CK(cudaMemcpy(hspec.p, H.data(), H.size() * sizeof(float2), cudaMemcpyHostToDevice));
-        hkey = k;
-        return hspec.as<float2>();
+        if (hspecs.size() >= 16) {   // evict the least recently used key
+            auto lru = std::min_element(hspecs.begin(), hspecs.end(),
+                                        [](const auto& a, const auto& b) { return a->last_use < b->last_use; });
+            track_graphs.clear();
+            hspecs.erase(lru);
+        }
+        auto e = std::make_unique<HSpec>();
+        e->key = k;
+        e->clen = cl;
+        e->last_use = ++hspec_clock;
+        e->buf.ensure(H.size() * sizeof(float2));
+        // a fresh buffer: stream-ordered before every kernel that will read it
+        CK(cudaMemcpyAsync(e->buf.p, H.data(), H.size() * sizeof(float2), cudaMemcpyHostToDevice, stream));
+        CK(cudaStreamSynchronize(stream));   // H is pageable and local
+        clen = cl;
+        const float2* p = e->buf.as<float2>();
+        hspecs.push_back(std::move(e));
+        return p;
     }
 };
 
@@ -1050,8 +1087,8 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
         ensure_dspec(ctx, w, N1, N2);
         S.groups = gd;
         S.outs = od;
-        launch_pass<0>(N1, N2, ctx->stream, S);
-        launch_pass<1>(N1, N2, ctx->stream, S);
+        launch_pass<0>(N1, N2, ctx->stream, S, ctx->cta_cap[0]);
+        launch_pass<1>(N1, N2, ctx->stream, S, ctx->cta_cap[1]);
         return;
     }
     ctx->ensure_pipeline(ring);
@@ -1083,11 +1120,11 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
             ++wt;
         }
         if (wv >= ring) CK(cudaStreamWaitEvent(sa, ctx->ev_b[size_t(r)], 0));
-        launch_pass<0>(N1, N2, sa, S);
+        launch_pass<0>(N1, N2, sa, S, ctx->cta_cap[0]);
         CK(cudaEventRecord(ctx->ev_a[size_t(r)], sa));
         cudaStream_t sb = ctx->one_stream ? sa : ctx->b_streams[size_t(wv % ns)];
         CK(cudaStreamWaitEvent(sb, ctx->ev_a[size_t(r)], 0));
-        launch_pass<1>(N1, N2, sb, S);
+        launch_pass<1>(N1, N2, sb, S, ctx->cta_cap[1]);
         CK(cudaEventRecord(ctx->ev_b[size_t(r)], sb));
     }
     for (int i = 0; i < ns; ++i)
@@ -1191,9 +1228,9 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
             ctx->b_streams.clear();
             ctx->n_streams = value > 0 ? value : 6;
         } else if (k == "cta_cap_a")
-            g_cta_cap[0] = int(value);
+            ctx->cta_cap[0] = int(value);
         else if (k == "cta_cap_b")
-            g_cta_cap[1] = int(value);
+            ctx->cta_cap[1] = int(value);
         else if (k == "one_stream")
             ctx->one_stream = value;
         else if (k == "discard")
@@ -1365,10 +1402,10 @@ int tdg_codeset_from_replicas(tdg_ctx* ctx, uint64_t window_len, uint64_t corr_l
         cs->n_codes = n_codes;
         DevBuf dd, du;
         dd.ensure(hd.size() * sizeof(float));
-        CK(cudaMemcpy(dd.p, hd.data(), hd.size() * sizeof(float), cudaMemcpyHostToDevice));
+        CK(cudaMemcpyAsync(dd.p, hd.data(), hd.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
         if (have_u) {
             du.ensure(hu.size() * sizeof(float));
-            CK(cudaMemcpy(du.p, hu.data(), hu.size() * sizeof(float), cudaMemcpyHostToDevice));
+            CK(cudaMemcpyAsync(du.p, hu.data(), hu.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
         }
         finish_codeset(ctx, cs.get(), dd.as<float>(), have_u ? du.as<float>() : nullptr, stride, lens, corr_len);
         *out = cs.release();
@@ -1516,37 +1553,62 @@ int tdg_windows_get_du(tdg_ctx* ctx, const tdg_windows* w, uint64_t slot, float*
 
 // ---- detection -------------------------------------------------------------
 namespace {
+// sel (optional): the code indices to detect, in output order (the
+// reference's detect over a span of TransformedCode pointers,
+// detector.hpp:103-106); nullptr = every code of the set.  Records are
+// [slot][k] for k < |sel|.  Only the stored pairs the selection touches are
+// correlated.
 void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float threshold, double fs, tdg_detection* out,
-                 bool sync = true) {
+                 bool sync = true, const std::vector<uint64_t>* sel = nullptr) {
     if (cs->window_len != w->W) fail(TDG_EINVAL, "batch_xcorr: mixed window shapes");
-    for (uint64_t i = 0; i < cs->n_codes; ++i)
-        if (w->W + cs->nlen[i] > cs->corr_len() + 1) fail(TDG_EINVAL, "batch_xcorr: window does not fit transform size");
     const uint64_t ns = w->used(), nc = cs->n_codes;
+    std::vector<uint64_t> all;
+    if (!sel) {
+        all.resize(nc);
+        for (uint64_t i = 0; i < nc; ++i) all[i] = i;
+        sel = &all;
+    }
+    const uint64_t nk = sel->size();
+    std::vector<char> want_pair((nc + 1) / 2, 0);
+    for (uint64_t c : *sel) {
+        if (c >= nc) fail(TDG_EINVAL, "detect: code index out of range");
+        if (w->W + cs->nlen[c] > cs->corr_len() + 1) fail(TDG_EINVAL, "batch_xcorr: window does not fit transform size");
+        want_pair[c / 2] = 1;
+    }
+    if (!nk) return;
+    // argmax keys [slot][code] of every code of a touched pair (the packed
+    // IFFT yields both codes of a pair)
     ctx->keys.ensure(ns * nc * sizeof(unsigned long long));
     CK(cudaMemsetAsync(ctx->keys.p, 0, ns * nc * sizeof(unsigned long long), ctx->stream));
     std::vector<CorrJob> jobs;
     unsigned long long* keys = ctx->keys.as<unsigned long long>();
     // code-pair-major: a group of kGroup stored pairs (whose spectra stay
     // L2-resident) sweeps every window slot before the next group starts
-    const uint64_t npairs = (nc + 1) / 2, G = tdg::kGroup;
-    for (uint64_t p0 = 0; p0 < npairs; p0 += G) {
+    std::vector<uint64_t> pairs;
+    for (uint64_t p = 0; p < want_pair.size(); ++p)
+        if (want_pair[p]) pairs.push_back(p);
+    const uint64_t G = tdg::kGroup;
+    for (uint64_t i0 = 0; i0 < pairs.size(); i0 += G) {
         for (uint64_t s = 0; s < ns; ++s)
-            for (uint64_t p = p0; p < std::min(npairs, p0 + G); ++p)
+            for (uint64_t i = i0; i < std::min<uint64_t>(pairs.size(), i0 + G); ++i) {
+                const uint64_t p = pairs[i];
                 jobs.push_back({s, p, keys + s * nc + 2 * p, 2 * p + 1 < nc ? keys + s * nc + 2 * p + 1 : nullptr,
                                 nullptr, nullptr});
+            }
     }
-    ctx->det_dev.ensure(ns * nc * sizeof(tdg_detection));
+    ctx->det_dev.ensure(ns * nk * sizeof(tdg_detection));
     // statistics: one CTA per (slot, code), slot-major so a window's d,u stay
     // in L2 across all codes
-    std::vector<tdg::StatsDesc> sd(ns * nc);
+    std::vector<tdg::StatsDesc> sd(ns * nk);
     for (uint64_t s = 0; s < ns; ++s)
-        for (uint64_t c = 0; c < nc; ++c) {
-            auto& x = sd[s * nc + c];
+        for (uint64_t k = 0; k < nk; ++k) {
+            const uint64_t c = (*sel)[k];
+            auto& x = sd[s * nk + k];
             x.d = w->d.as<float>() + s * w->W;
             x.u = w->u.as<float>() + s * w->W;
             x.dc = cs->rep.as<float>() + c * cs->rep_cap;
             x.key = keys + s * nc + c;
-            x.out = ctx->det_dev.as<tdg_detection>() + s * nc + c;
+            x.out = ctx->det_dev.as<tdg_detection>() + s * nk + k;
             x.nonzero_len = uint32_t(cs->nlen[c]);
             x.energy = cs->energy[c];
             x.window_start = w->start[s];
@@ -1565,17 +1627,32 @@ void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float thre
     // behind it and takes SM slots from the persistent passes)
     launch_stats(ctx, sdd, sd.size(), uint32_t(w->W), fs, threshold);
     if (out) {
-        CK(cudaMemcpyAsync(out, ctx->det_dev.p, ns * nc * sizeof(tdg_detection), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(out, ctx->det_dev.p, ns * nk * sizeof(tdg_detection), cudaMemcpyDeviceToHost, ctx->stream));
         if (sync) CK(cudaStreamSynchronize(ctx->stream));
     }
 }
 }  // namespace
 
 int tdg_detect(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float threshold, double sample_rate,
-               tdg_detection* out) {
+               tdg_detection* out, uint64_t out_cap) {
     return guard([&] {
         CK(cudaSetDevice(ctx->device));
+        if (out && out_cap < w->used() * cs->n_codes) fail(TDG_EINVAL, "detect: output capacity too small");
         detect_impl(ctx, w, cs, threshold, sample_rate, out);
+    });
+}
+
+int tdg_detect_codes(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const int64_t* idx, uint64_t n_idx,
+                     float threshold, double sample_rate, tdg_detection* out, uint64_t out_cap) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        std::vector<uint64_t> sel(n_idx);
+        for (uint64_t i = 0; i < n_idx; ++i) {
+            if (idx[i] < 0 || uint64_t(idx[i]) >= cs->n_codes) fail(TDG_EINVAL, "detect: code index out of range");
+            sel[i] = uint64_t(idx[i]);
+        }
+        if (out && out_cap < w->used() * n_idx) fail(TDG_EINVAL, "detect: output capacity too small");
+        detect_impl(ctx, w, cs, threshold, sample_rate, out, true, &sel);
     });
 }
 
@@ -1588,19 +1665,26 @@ int tdg_batch_xcorr(tdg_ctx* ctx, tdg_windows* w, uint64_t slot, const tdg_codes
         std::vector<int64_t> codes(idx, idx + n_idx);
         for (int64_t c : codes)
             if (c < 0 || uint64_t(c) >= cs->n_codes) fail(TDG_EINVAL, "code index out of range");
+        // one row per distinct code (a code requested twice gets the same row
+        // twice, like the reference's per-index loop, detector.cpp:116-118);
+        // one job per stored pair touched
+        std::map<uint64_t, uint64_t> row_of;   // code -> row of xc
+        for (int64_t c : codes) row_of.emplace(uint64_t(c), 0);
+        uint64_t nr = 0;
+        for (auto& kv : row_of) kv.second = nr++;
         DevBuf xc;
-        xc.ensure(std::max<uint64_t>(1, n_idx) * w->W * sizeof(float));
-        // one job per stored pair touched; rows for the requested codes only
+        xc.ensure(std::max<uint64_t>(1, nr) * w->W * sizeof(float));
         std::map<uint64_t, std::pair<float*, float*>> per_pair;
-        for (uint64_t i = 0; i < n_idx; ++i) {
-            const uint64_t c = uint64_t(codes[i]);
+        for (auto& [c, r] : row_of) {
             auto& pp = per_pair[c / 2];
-            (c % 2 ? pp.second : pp.first) = xc.as<float>() + i * w->W;
+            (c % 2 ? pp.second : pp.first) = xc.as<float>() + r * w->W;
         }
         std::vector<CorrJob> jobs;
         for (auto& [p, rows] : per_pair) jobs.push_back({slot, p, nullptr, nullptr, rows.first, rows.second});
         run_correlations(ctx, w, cs, jobs, true);
-        CK(cudaMemcpyAsync(out, xc.p, n_idx * w->W * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        for (uint64_t i = 0; i < n_idx; ++i)
+            CK(cudaMemcpyAsync(out + i * w->W, xc.as<float>() + row_of[uint64_t(codes[i])] * w->W,
+                               w->W * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
     });
 }
@@ -2003,6 +2087,50 @@ int tdg_track_ring(tdg_ctx* ctx, tdg_ring* r, const tdg_demod_config* cfg, const
         if (n_tasks == 0) return;
         if (r->device != ctx->device) fail(TDG_EINVAL, "track: ring and context on different devices");
         track_impl(ctx, cfg, SampleSource::of(r), tasks, n_tasks, cs, threshold, out, sync != 0);
+    });
+}
+
+// FP32 peak of the current device at its current clock (bench.py's roofline
+// denominator): TFLOP/s of scalar FFMA and of packed FFMA2 (2 flops per FMA
+// lane), best of 5 timed launches after a warm-up.
+int tdg_fp32_peak(int device, double* ffma_tflops, double* ffma2_tflops) {
+    return guard([&] {
+        CK(cudaSetDevice(device));
+        const int sms = num_sms();
+        DevBuf out;
+        out.ensure(64);
+        CK(cudaMemset(out.p, 0, 64));
+        cudaStream_t st;
+        CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        const int iters = 2048, threads = 512, blocks = sms * 4;
+        double best1 = 0, best2 = 0;
+        for (int rep = 0; rep < 6; ++rep) {
+            float ms = 0;
+            CK(cudaEventRecord(e0, st));
+            tdg::k_peak_ffma<<<blocks, threads, 0, st>>>(out.as<float>(), iters);
+            CK(cudaEventRecord(e1, st));
+            CK(cudaEventSynchronize(e1));
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            const double f1 = double(blocks) * threads * iters * 64 * 2 / (ms * 1e-3) / 1e12;
+            CK(cudaEventRecord(e0, st));
+            tdg::k_peak_ffma2<<<blocks, threads, 0, st>>>(out.as<float>(), iters);
+            CK(cudaEventRecord(e1, st));
+            CK(cudaEventSynchronize(e1));
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            const double f2 = double(blocks) * threads * iters * 64 * 4 / (ms * 1e-3) / 1e12;
+            if (rep) {
+                best1 = std::max(best1, f1);
+                best2 = std::max(best2, f2);
+            }
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaStreamDestroy(st);
+        if (ffma_tflops) *ffma_tflops = best1;
+        if (ffma2_tflops) *ffma2_tflops = best2;
     });
 }
 

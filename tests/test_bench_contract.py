@@ -34,3 +34,16 @@ def test_paper_perf_ratio_arithmetic():
     ratio = (1.0 / corr_per_s) / (bench.W / bench.FS)
     assert abs(ratio - 2.247e-5) < 1e-8
     assert int(math.floor(0.5 / ratio)) == 22_250
+
+
+def test_roofline_formula():
+    # bound fp32, frac = achieved / peak, attainable = min(HBM roof, FP32 roof)
+    r = bench.roofline(6336, 13.0, 150.0, 6556.2, bench.bytes_per_corr(9, 64))
+    assert r["bound"] == "fp32" and r["unit"] == "TFLOP/s"
+    assert abs(r["achieved"] - 6336 * 47.6e6 / 13e-3 / 1e12) < 1e-9
+    assert abs(r["frac"] - r["achieved"] / 150.0) < 1e-12
+    fp32_roof = 150e12 / 47.6e6
+    hbm_roof = 6556.2e9 / bench.bytes_per_corr(9, 64)
+    assert abs(r["attainable_corr_per_s"] - min(fp32_roof, hbm_roof)) < 1e-6
+    assert abs(r["frac_of_attainable"] - (6336 / 13e-3) / min(fp32_roof, hbm_roof)) < 1e-12
+    assert abs(r["hbm"]["frac"] - bench.bytes_per_corr(9, 64) * 6336 / 13e-3 / 6556.2e9) < 1e-12

@@ -42,7 +42,7 @@ def main():
     def device():
         capi._check(lib.tdg_demodulate_device(ctx.handle, win._h, ctypes.byref(cfg), capi._ptr(bins), bins.size,
                                               ctypes.c_void_p(iq_dev.data_ptr()), n, 0, bench.ADV, bench.N_WIN))
-        capi._check(lib.tdg_detect(ctx.handle, win._h, cs._h, 0.25, bench.FS, None))
+        capi._check(lib.tdg_detect(ctx.handle, win._h, cs._h, 0.25, bench.FS, None, 0))
 
     def search_ring(start):
         capi._check(lib.tdg_search_ring(ctx.handle, ring._h, ctypes.byref(cfg), capi._ptr(bins), bins.size, start,

@@ -12,7 +12,7 @@ lscpu > $OUT/lscpu.txt 2>&1
 for w in $WHAT; do
 case $w in
 tests)
-  timeout 900 python -m pytest tests -x -q -m gpu > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log ;;
+  TDG_PARITY_OUT=$OUT timeout 1500 python -m pytest tests -x -q -m gpu -rs --durations=15 > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log ;;
 smoke)
   timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log ;;
 bench)

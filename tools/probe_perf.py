@@ -39,7 +39,7 @@ ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=
 def step():
     capi._check(lib.tdg_demodulate_device(ctx.handle, win._h, ctypes.byref(cfg), capi._ptr(bins), bins.size,
                                           ctypes.c_void_p(iq_t.data_ptr()), total, 0, adv, n_win))
-    capi._check(lib.tdg_detect(ctx.handle, win._h, cs._h, 0.25, cfg.mod.sample_rate, None))
+    capi._check(lib.tdg_detect(ctx.handle, win._h, cs._h, 0.25, cfg.mod.sample_rate, None, 0))
 
 
 for _ in range(2):

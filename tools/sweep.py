@@ -38,18 +38,18 @@ def main():
             k, v = kv.split("=")
             ctx.set_option(k, int(v))
         for _ in range(2):
-            capi._check(lib.tdg_detect(ctx.handle, win._h, cs._h, 0.25, bench.FS, None))
+            capi._check(lib.tdg_detect(ctx.handle, win._h, cs._h, 0.25, bench.FS, None, 0))
         ctx.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = 5
         e0.record(stream)
         for _ in range(reps):
-            capi._check(lib.tdg_detect(ctx.handle, win._h, cs._h, 0.25, bench.FS, None))
+            capi._check(lib.tdg_detect(ctx.handle, win._h, cs._h, 0.25, bench.FS, None, 0))
         e1.record(stream)
         ctx.synchronize()
         ms = e0.elapsed_time(e1) / reps
         out = (ctypes.c_char * (n_units * 64))()
-        capi._check(lib.tdg_detect(ctx.handle, win._h, cs._h, 0.25, bench.FS, out))
+        capi._check(lib.tdg_detect(ctx.handle, win._h, cs._h, 0.25, bench.FS, out, out.size))
         h = hash(bytes(out))
         same = "" if ref is None else (" same-detections" if h == ref else " DIFFERENT-detections")
         ref = h if ref is None else ref
