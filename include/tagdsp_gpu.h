@@ -74,6 +74,13 @@ int tdg_codeset_prepare(tdg_ctx* ctx, const tdg_demod_config* cfg, uint64_t wind
  * (replica_u may be NULL -> support measured on d).  corr_len is the
  * reference's transform length and is only used for its precondition
  * (window_len + n <= corr_len + 1, else TDG_EINVAL). */
+/* prepare_code for n_codes more codes of the same configuration, appended to
+ * cs (indices n .. n + n_codes - 1): only the stored pairs the new codes touch
+ * are transformed (all of them if a longer support needs a longer transform);
+ * device buffers grow by doubling.  TDG_EINVAL for a code set made by
+ * make_transformed or prepared with another configuration. */
+int tdg_codeset_append(tdg_ctx* ctx, tdg_codeset* cs, const tdg_demod_config* cfg, const uint8_t* bits,
+                       uint64_t n_codes);
 int tdg_codeset_from_replicas(tdg_ctx* ctx, uint64_t window_len, uint64_t corr_len,
                               const float* const* replica_d, const float* const* replica_u,
                               const uint64_t* lengths, uint64_t n_codes, tdg_codeset** out);
@@ -107,6 +114,8 @@ int tdg_demodulate_device(tdg_ctx* ctx, tdg_windows* win, const tdg_demod_config
 int tdg_windows_set_du(tdg_ctx* ctx, tdg_windows* w, uint64_t slot, const float* d, const float* u,
                        int64_t window_start);
 int tdg_windows_get_du(tdg_ctx* ctx, const tdg_windows* w, uint64_t slot, float* d, float* u);
+/* DetectionConfig::window_start of a slot whose d,u are already on the device. */
+int tdg_windows_set_start(tdg_ctx* ctx, tdg_windows* w, uint64_t slot, int64_t window_start);
 
 /* ---- detection -----------------------------------------------------------
  * detect (proj/src/detector.cpp:167-206) for every slot x code: one forward
@@ -185,6 +194,40 @@ int tdg_search_ring(tdg_ctx* ctx, tdg_ring* ring, const tdg_demod_config* cfg, c
 int tdg_track_ring(tdg_ctx* ctx, tdg_ring* ring, const tdg_demod_config* cfg, const tdg_track_task* tasks,
                    uint64_t n_tasks, const tdg_codeset* cs, float threshold, tdg_detection* out, int sync);
 
+/* ---- span-level functions of the reference API ----------------------------
+ * Host arrays in and out, each a device round trip; the drop-in
+ * (include/tagdsp_b200, libtagdsp_b200.so) maps the reference's free
+ * functions onto them.  Complex arrays are interleaved float pairs. */
+/* PlanCache::forward / inverse (proj/src/fft.cpp:46-67): C2C DFT of any
+ * {2,3,5,7}-smooth length n (else TDG_ERANGE); inverse = +sign and 1/n. */
+int tdg_fft(tdg_ctx* ctx, const float* in, float* out, uint64_t n, int inverse);
+/* convert (proj/src/dsp.cpp:9-16): n_int16 interleaved I,Q -> n_int16/2 complex. */
+int tdg_convert(tdg_ctx* ctx, const int16_t* iq, uint64_t n_int16, float* out);
+/* mix (proj/src/dsp.cpp:18-33), in place; no-op for lo_freq == 0. */
+int tdg_mix(tdg_ctx* ctx, float* x, uint64_t n, double lo_freq, int64_t start_index, double sample_rate);
+/* full linear convolution of x (nx complex) with h (nh complex) -> nx+nh-1
+ * complex (overlap_add_filter, proj/src/dsp.cpp:137-145, ConvMode::Full). */
+int tdg_convolve(tdg_ctx* ctx, const float* x, uint64_t nx, const float* h, uint64_t nh, float* out);
+/* demodulate (proj/src/dsp.cpp:147-157). */
+int tdg_discriminate(tdg_ctx* ctx, const float* f1, const float* f0, uint64_t n, float eps, float* d, float* u);
+/* find_peak (proj/src/detector.cpp:122-134): first index of max |xc|, signed value. */
+int tdg_find_peak(tdg_ctx* ctx, const float* xc, uint64_t n, uint64_t* j, float* value);
+/* statistics (proj/src/detector.cpp:147-165) of replica dc (n) at lag j of d,u (W). */
+int tdg_statistics(tdg_ctx* ctx, const float* d, const float* u, uint64_t W, const float* dc, uint64_t n,
+                   uint64_t j, float* w_c, float* q, float* p_c, int* partial);
+/* demodulate_signal (proj/src/dsp.cpp:159-191) of n complex samples at
+ * lo_freq into slot 0 of win (window length n). */
+int tdg_demodulate_signal(tdg_ctx* ctx, tdg_windows* win, const tdg_demod_config* cfg, double lo_freq,
+                          const float* x, uint64_t n, int64_t start_index);
+/* DetectTimings (proj/include/tagdsp/detector.hpp:95-98) of the last detect
+ * on this context when option "detect_timings" is 1 (CUDA events). */
+int tdg_detect_timings(tdg_ctx* ctx, double* correlation_s, double* peak_stats_s);
+
+/* detection_json_line (proj/src/recording.cpp:228-242): the record as the
+ * reference's JSON line (byte-identical: same nlohmann::json dump) into out
+ * (cap bytes incl. the terminator; *len = its length; TDG_EINVAL if short). */
+int tdg_detection_json_line(const tdg_detection* det, const char* tag_id, char* out, uint64_t cap, uint64_t* len);
+
 /* Tuning / profiling knobs (0 = default): "wave_pairs" (8), "ring" (3),
  * "n_streams" (6), "discard" (1), "fwd_wave" (32), "one_stream",
  * "cta_cap_a" / "cta_cap_b" (CTAs per SM of the two correlation passes of
@@ -193,7 +236,9 @@ int tdg_track_ring(tdg_ctx* ctx, tdg_ring* ring, const tdg_demod_config* cfg, co
  * every launch; read back with tdg_kernel_time), "track_graphs" (default 1:
  * tdg_track / tdg_track_device batches that fit one correlation wave are
  * captured as a CUDA graph on their second call with the same shape and
- * replayed from the third; 0 = always issue the launches).  Setting any
+ * replayed from the third; 0 = always issue the launches), "detect_timings"
+ * (1 = record the correlation / statistics split of every detect, read with
+ * tdg_detect_timings).  Setting any
  * option drops the context's captured graphs. */
 int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value);
 /* Launch count and summed device time (ms) of one kernel family since the

@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <cstdio>
+#include <fstream>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -20,6 +22,7 @@
 #include "tagdsp/dsp.hpp"
 #include "tagdsp/harness.hpp"
 #include "tagdsp/recording.hpp"
+#include "tagdsp/scheduler.hpp"
 #include "tagdsp_gpu_types.h"
 
 using namespace tagdsp;
@@ -598,6 +601,108 @@ double tdref_track_bench(const int16_t* iq, uint64_t n_complex, int64_t stream_s
         elapsed = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     });
     return rc ? -double(rc) : elapsed;
+}
+
+// detect_recording / simulate_recording (proj/src/recording.cpp:258-389) on
+// a recording file + run-config file, output as the reference's JSON lines
+// (detection_json_line / event_json_line) -- the oracle side of the drop-in
+// tests (tests/test_gpu_dropin.py).
+int tdref_run_detect_recording(const char* rec_path, const char* cfg_path, const char* out_path) {
+    return guard([&] {
+        auto rec = read_recording(rec_path);
+        auto cfg = load_run_config(cfg_path);
+        auto dets = detect_recording(rec, cfg);
+        std::ofstream out(out_path);
+        for (const auto& d : dets) out << detection_json_line(d) << "\n";
+    });
+}
+
+int tdref_run_simulate(const char* rec_path, const char* cfg_path, const char* out_path, double compute_ratio,
+                       uint64_t* detections, uint64_t* misses) {
+    return guard([&] {
+        auto rec = read_recording(rec_path);
+        auto cfg = load_run_config(cfg_path);
+        auto res = simulate_recording(rec, cfg, compute_ratio);
+        std::ofstream out(out_path);
+        for (const auto& e : res.events) out << event_json_line(e) << "\n";
+        *detections = res.detections;
+        *misses = res.misses;
+    });
+}
+
+// write_recording / read_recording / detection_json_line
+// (proj/src/recording.cpp:23-64,228-242) for the recording-format cross-checks
+int tdref_write_recording(const char* path, const int16_t* iq, uint64_t n_complex, double sample_rate,
+                          int64_t start_time, double center_freq, const char* creator) {
+    return guard([&] {
+        RecordingFile rec;
+        rec.block.samples.assign(iq, iq + 2 * n_complex);
+        rec.block.sample_rate = sample_rate;
+        rec.block.start_time = start_time;
+        rec.center_freq = center_freq;
+        rec.creator = creator;
+        write_recording(path, rec);
+    });
+}
+
+int tdref_read_recording(const char* path, int16_t* iq, uint64_t cap_int16, uint64_t* n_complex, double* sample_rate,
+                         int64_t* start_time, double* center_freq, char* creator, uint64_t creator_cap) {
+    return guard([&] {
+        auto rec = read_recording(path);
+        *n_complex = rec.block.num_complex();
+        if (rec.block.samples.size() > cap_int16) throw std::runtime_error("read_recording: buffer too small");
+        std::memcpy(iq, rec.block.samples.data(), rec.block.samples.size() * sizeof(int16_t));
+        *sample_rate = rec.block.sample_rate;
+        *start_time = rec.block.start_time;
+        *center_freq = rec.center_freq;
+        std::snprintf(creator, creator_cap, "%s", rec.creator.c_str());
+    });
+}
+
+int tdref_detection_json_line(const tdg_detection* r, const char* tag_id, char* out, uint64_t cap) {
+    return guard([&] {
+        Detection d;
+        d.tag_id = tag_id;
+        d.peak_index = size_t(r->peak_index);
+        d.subsample_offset = r->subsample_offset;
+        d.toa_seconds = r->toa_seconds;
+        d.peak_value = r->peak_value;
+        d.w_c = r->w_c;
+        d.q = r->q;
+        d.p_c = r->p_c;
+        d.score = r->score;
+        d.accepted = r->accepted != 0;
+        d.partial = r->partial != 0;
+        std::snprintf(out, cap, "%s", detection_json_line(d).c_str());
+    });
+}
+
+// CircularBuffer (proj/src/scheduler.cpp:7-45): create / push / read / bounds,
+// the oracle of the device ring tdg_ring_* (tests/test_gpu_ring.py)
+void* tdref_ring_new(uint64_t capacity) { return new CircularBuffer(size_t(capacity)); }
+void tdref_ring_free(void* r) { delete static_cast<CircularBuffer*>(r); }
+int tdref_ring_push(void* r, const int16_t* iq, uint64_t n_complex, int64_t start, int64_t* ev_begin, int64_t* ev_end,
+                    int32_t* gap) {
+    return guard([&] {
+        RawSampleBlock blk;
+        blk.samples.assign(iq, iq + 2 * n_complex);
+        blk.start_time = start;
+        auto res = static_cast<CircularBuffer*>(r)->push(blk);
+        *ev_begin = res.evicted_begin;
+        *ev_end = res.evicted_end;
+        *gap = res.gap ? 1 : 0;
+    });
+}
+int tdref_ring_read(void* r, int64_t start, int64_t end, int16_t* out, int32_t* ok) {
+    return guard([&] {
+        std::vector<int16_t> v;
+        *ok = static_cast<CircularBuffer*>(r)->read(start, end, v) ? 1 : 0;
+        if (*ok) std::memcpy(out, v.data(), v.size() * sizeof(int16_t));
+    });
+}
+void tdref_ring_bounds(void* r, int64_t* head, int64_t* tail) {
+    *head = static_cast<CircularBuffer*>(r)->head();
+    *tail = static_cast<CircularBuffer*>(r)->tail();
 }
 
 }  // extern "C"

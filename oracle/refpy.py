@@ -66,6 +66,21 @@ def lib():
             "tdref_search_bench_shared": (ctypes.c_double, [_P, _U64, _I64, ctypes.POINTER(DemodConfig), _P, _U64,
                                                             _P, _U64, _U64, _U64, _U64, ctypes.c_float, ctypes.c_int,
                                                             ctypes.c_int, _P, _P]),
+            "tdref_run_detect_recording": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p]),
+            "tdref_run_simulate": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_double,
+                                                  ctypes.POINTER(_U64), ctypes.POINTER(_U64)]),
+            "tdref_write_recording": (ctypes.c_int, [ctypes.c_char_p, _P, _U64, ctypes.c_double, _I64,
+                                                     ctypes.c_double, ctypes.c_char_p]),
+            "tdref_read_recording": (ctypes.c_int, [ctypes.c_char_p, _P, _U64, ctypes.POINTER(_U64),
+                                                    ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_I64),
+                                                    ctypes.POINTER(ctypes.c_double), ctypes.c_char_p, _U64]),
+            "tdref_detection_json_line": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.c_char_p, _U64]),
+            "tdref_ring_new": (_P, [_U64]),
+            "tdref_ring_free": (None, [_P]),
+            "tdref_ring_push": (ctypes.c_int, [_P, _P, _U64, _I64, ctypes.POINTER(_I64), ctypes.POINTER(_I64),
+                                               ctypes.POINTER(ctypes.c_int32)]),
+            "tdref_ring_read": (ctypes.c_int, [_P, _I64, _I64, _P, ctypes.POINTER(ctypes.c_int32)]),
+            "tdref_ring_bounds": (None, [_P, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
             "tdref_track_bench": (ctypes.c_double, [_P, _U64, _I64, ctypes.POINTER(DemodConfig), _P, _U64, _U64, _P,
                                                     _P, _U64, ctypes.c_float, _P]),
         }
@@ -306,3 +321,69 @@ def track_bench(iq, stream_start, cfg, bits, window_len, starts, code_idx, thres
     if t < 0:
         _ck(int(-t))
     return t, out
+
+
+def run_detect_recording(rec_path, cfg_path, out_path):
+    """The reference's detect_recording over a recording file, JSON lines out."""
+    _ck(lib().tdref_run_detect_recording(str(rec_path).encode(), str(cfg_path).encode(), str(out_path).encode()))
+
+
+def run_simulate(rec_path, cfg_path, out_path, compute_ratio):
+    """The reference's simulate_recording; event JSON lines out; returns (detections, misses)."""
+    d, m = _U64(), _U64()
+    _ck(lib().tdref_run_simulate(str(rec_path).encode(), str(cfg_path).encode(), str(out_path).encode(),
+                                 float(compute_ratio), ctypes.byref(d), ctypes.byref(m)))
+    return d.value, m.value
+
+
+def write_recording(path, iq, sample_rate, start_time=0, center_freq=0.0, creator=""):
+    iq = np.ascontiguousarray(iq, dtype=np.int16)
+    _ck(lib().tdref_write_recording(str(path).encode(), _p(iq), iq.size // 2, float(sample_rate), int(start_time),
+                                    float(center_freq), creator.encode()))
+
+
+def read_recording(path, cap_complex):
+    out = np.empty(2 * cap_complex, np.int16)
+    n, rate, start, cf = _U64(), ctypes.c_double(), _I64(), ctypes.c_double()
+    creator = ctypes.create_string_buffer(4096)
+    _ck(lib().tdref_read_recording(str(path).encode(), _p(out), out.size, ctypes.byref(n), ctypes.byref(rate),
+                                   ctypes.byref(start), ctypes.byref(cf), creator, 4096))
+    return out[:2 * n.value], rate.value, start.value, cf.value, creator.value.decode()
+
+
+def detection_json_line(rec, tag_id):
+    r = np.ascontiguousarray(np.atleast_1d(rec).astype(DETECTION_DTYPE))
+    buf = ctypes.create_string_buffer(4096)
+    _ck(lib().tdref_detection_json_line(_p(r), tag_id.encode(), buf, 4096))
+    return buf.value.decode()
+
+
+class Ring:
+    """The reference CircularBuffer (proj/src/scheduler.cpp:7-45)."""
+
+    def __init__(self, capacity):
+        self.h = lib().tdref_ring_new(int(capacity))
+
+    def push(self, iq, start):
+        iq = np.ascontiguousarray(iq, dtype=np.int16)
+        b, e, g = _I64(), _I64(), ctypes.c_int32()
+        _ck(lib().tdref_ring_push(self.h, _p(iq), iq.size // 2, int(start), ctypes.byref(b), ctypes.byref(e),
+                                  ctypes.byref(g)))
+        return b.value, e.value, bool(g.value)
+
+    def read(self, start, end):
+        out = np.empty(2 * max(0, int(end) - int(start)), np.int16)
+        ok = ctypes.c_int32()
+        _ck(lib().tdref_ring_read(self.h, int(start), int(end), _p(out), ctypes.byref(ok)))
+        return out if ok.value else None
+
+    def bounds(self):
+        h, t = _I64(), _I64()
+        lib().tdref_ring_bounds(self.h, ctypes.byref(h), ctypes.byref(t))
+        return h.value, t.value
+
+    def __del__(self):
+        try:
+            lib().tdref_ring_free(self.h)
+        except Exception:
+            pass

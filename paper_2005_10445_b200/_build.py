@@ -11,8 +11,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtagdsp_gpu.so")
-SOURCES = ["tagdsp_gpu.cu"]
-DEPS = SOURCES + ["kernels.cuh", "codelets.cuh", "corr_v3.cuh", "tma.cuh", "peak.cuh"]
+SOURCES = ["tagdsp_gpu.cu", "records.cpp"]
+# nlohmann/json (header-only, the version the oracle compiles the reference with)
+NLOHMANN = os.environ.get("NLOHMANN", "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty")
+DEPS = SOURCES + ["kernels.cuh", "codelets.cuh", "corr_v3.cuh", "tma.cuh", "peak.cuh", "generic.cuh"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 
@@ -33,22 +35,29 @@ def stale():
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force=False, verbose=False):
-    if not force and not stale():
+def build(force=False, verbose=False, defines=(), out=None):
+    """Build the library (defines: extra -D flags of a layout variant, out:
+    another path -- tools/ab_libs.sh A/B builds go to abtest/)."""
+    target = out or LIB
+    if not force and not defines and out is None and not stale():
         return LIB
-    cmd = [_nvcc()] + NVCC_FLAGS + ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-o", LIB] + \
-        [os.path.join(CSRC, s) for s in SOURCES]
+    cmd = [_nvcc()] + NVCC_FLAGS + ["-D" + d for d in defines] + \
+        ["-I" + os.path.join(ROOT, "include"), "-I" + CSRC, "-I" + NLOHMANN, "-o", target] + [os.path.join(CSRC, s) for s in SOURCES]
     res = subprocess.run(cmd, capture_output=True, text=True)
-    log = os.path.join(HERE, "build.log")
+    log = os.path.join(HERE, "build.log") if out is None else target + ".log"
     with open(log, "w") as f:
         f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
     if res.returncode != 0:
         sys.stderr.write(res.stderr[-4000:])
         raise RuntimeError("nvcc failed building libtagdsp_gpu.so (see %s)" % log)
     if verbose:
-        print("built", LIB)
-    return LIB
+        print("built", target)
+    return target
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    # python _build.py [--force] [-DNAME=V ...] [-o path]
+    args = sys.argv[1:]
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    out = args[args.index("-o") + 1] if "-o" in args else None
+    build(force="--force" in args, verbose=True, defines=defs, out=out)

@@ -59,6 +59,7 @@ _PROTOS = {
     "tdg_corr_len": (_U64, [_U64, _U64]),
     "tdg_codeset_prepare": (ctypes.c_int, [_P, ctypes.POINTER(DemodConfig), _U64, _P, _U64, ctypes.POINTER(_P)]),
     "tdg_codeset_from_replicas": (ctypes.c_int, [_P, _U64, _U64, _P, _P, _P, _U64, ctypes.POINTER(_P)]),
+    "tdg_codeset_append": (ctypes.c_int, [_P, _P, ctypes.POINTER(DemodConfig), _P, _U64]),
     "tdg_codeset_destroy": (None, [_P]),
     "tdg_codeset_size": (_U64, [_P]),
     "tdg_codeset_info": (ctypes.c_int, [_P, _U64, ctypes.POINTER(_U64), ctypes.POINTER(ctypes.c_float),
@@ -71,6 +72,7 @@ _PROTOS = {
                                              _U64]),
     "tdg_windows_set_du": (ctypes.c_int, [_P, _P, _U64, _P, _P, _I64]),
     "tdg_windows_get_du": (ctypes.c_int, [_P, _P, _U64, _P, _P]),
+    "tdg_windows_set_start": (ctypes.c_int, [_P, _P, _U64, _I64]),
     "tdg_detect": (ctypes.c_int, [_P, _P, _P, ctypes.c_float, ctypes.c_double, _P, _U64]),
     "tdg_detect_codes": (ctypes.c_int, [_P, _P, _P, _P, _U64, ctypes.c_float, ctypes.c_double, _P, _U64]),
     "tdg_batch_xcorr": (ctypes.c_int, [_P, _P, _U64, _P, _P, _U64, _P]),
@@ -92,6 +94,18 @@ _PROTOS = {
     "tdg_set_option": (ctypes.c_int, [_P, ctypes.c_char_p, _I64]),
     "tdg_kernel_time": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.POINTER(_U64), ctypes.POINTER(ctypes.c_double)]),
     "tdg_kernel_time_reset": (ctypes.c_int, [_P]),
+    "tdg_fft": (ctypes.c_int, [_P, _P, _P, _U64, ctypes.c_int]),
+    "tdg_convert": (ctypes.c_int, [_P, _P, _U64, _P]),
+    "tdg_mix": (ctypes.c_int, [_P, _P, _U64, ctypes.c_double, _I64, ctypes.c_double]),
+    "tdg_convolve": (ctypes.c_int, [_P, _P, _U64, _P, _U64, _P]),
+    "tdg_discriminate": (ctypes.c_int, [_P, _P, _P, _U64, ctypes.c_float, _P, _P]),
+    "tdg_find_peak": (ctypes.c_int, [_P, _P, _U64, ctypes.POINTER(_U64), ctypes.POINTER(ctypes.c_float)]),
+    "tdg_statistics": (ctypes.c_int, [_P, _P, _P, _U64, _P, _U64, _U64, ctypes.POINTER(ctypes.c_float),
+                                      ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_float),
+                                      ctypes.POINTER(ctypes.c_int)]),
+    "tdg_demodulate_signal": (ctypes.c_int, [_P, _P, ctypes.POINTER(DemodConfig), ctypes.c_double, _P, _U64, _I64]),
+    "tdg_detect_timings": (ctypes.c_int, [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
+    "tdg_detection_json_line": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.c_char_p, _U64, ctypes.POINTER(_U64)]),
     "tdg_fp32_peak": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]),
 }
 EXPORTED_SYMBOLS = sorted(_PROTOS)
@@ -215,6 +229,11 @@ class CodeSet:
         _check(lib().tdg_codeset_prepare(ctx.handle, ctypes.byref(cfg), int(window_len), _ptr(bits),
                                          bits.shape[0], ctypes.byref(h)))
         return cls(ctx, h, int(window_len))
+
+    def append(self, cfg, bits):
+        """prepare_code for more codes of the same configuration (appended)."""
+        bits = np.ascontiguousarray(np.atleast_2d(bits), dtype=np.uint8)
+        _check(lib().tdg_codeset_append(self.ctx.handle, self._h, ctypes.byref(cfg), _ptr(bits), bits.shape[0]))
 
     @classmethod
     def from_replicas(cls, ctx, window_len, corr_len, replicas_d, replicas_u=None):
@@ -454,3 +473,79 @@ def track_ring(ctx, ring, cfg, starts, code_idx, codes, threshold=0.25):
     _check(lib().tdg_track_ring(ctx.handle, ring._h, ctypes.byref(cfg), _ptr(tasks), tasks.size, codes._h,
                                 float(threshold), _ptr(out), 1))
     return out
+
+
+# ---- span-level functions (reference free functions on host arrays) --------
+def fft(ctx, x, inverse=False):
+    """PlanCache::forward / inverse (proj/src/fft.cpp:46-67) on the GPU."""
+    x = np.ascontiguousarray(x, dtype=np.complex64)
+    out = np.empty_like(x)
+    _check(lib().tdg_fft(ctx.handle, _ptr(x), _ptr(out), x.size, int(bool(inverse))))
+    return out
+
+
+def convert(ctx, iq):
+    iq = np.ascontiguousarray(iq, dtype=np.int16)
+    out = np.empty(iq.size // 2, np.complex64)
+    _check(lib().tdg_convert(ctx.handle, _ptr(iq), iq.size, _ptr(out)))
+    return out
+
+
+def mix(ctx, x, lo_freq, start_index, sample_rate):
+    x = np.array(x, dtype=np.complex64, copy=True)
+    _check(lib().tdg_mix(ctx.handle, _ptr(x), x.size, float(lo_freq), int(start_index), float(sample_rate)))
+    return x
+
+
+def convolve(ctx, x, h):
+    x = np.ascontiguousarray(x, dtype=np.complex64)
+    h = np.ascontiguousarray(h, dtype=np.complex64)
+    out = np.empty(max(0, x.size + h.size - 1) if x.size else 0, np.complex64)
+    _check(lib().tdg_convolve(ctx.handle, _ptr(x), x.size, _ptr(h), h.size, _ptr(out)))
+    return out
+
+
+def discriminate(ctx, f1, f0, eps=1e-12):
+    f1 = np.ascontiguousarray(f1, dtype=np.complex64)
+    f0 = np.ascontiguousarray(f0, dtype=np.complex64)
+    d = np.empty(f1.size, np.float32)
+    u = np.empty(f1.size, np.float32)
+    _check(lib().tdg_discriminate(ctx.handle, _ptr(f1), _ptr(f0), f1.size, float(eps), _ptr(d), _ptr(u)))
+    return d, u
+
+
+def find_peak(ctx, xc):
+    xc = np.ascontiguousarray(xc, dtype=np.float32)
+    j, v = _U64(), ctypes.c_float()
+    _check(lib().tdg_find_peak(ctx.handle, _ptr(xc), xc.size, ctypes.byref(j), ctypes.byref(v)))
+    return j.value, v.value
+
+
+def statistics(ctx, d, u, dc, j):
+    d = np.ascontiguousarray(d, dtype=np.float32)
+    u = np.ascontiguousarray(u, dtype=np.float32)
+    dc = np.ascontiguousarray(dc, dtype=np.float32)
+    w, q, p, part = ctypes.c_float(), ctypes.c_float(), ctypes.c_float(), ctypes.c_int()
+    _check(lib().tdg_statistics(ctx.handle, _ptr(d), _ptr(u), d.size, _ptr(dc), dc.size, int(j), ctypes.byref(w),
+                                ctypes.byref(q), ctypes.byref(p), ctypes.byref(part)))
+    return {"w_c": w.value, "q": q.value, "p_c": p.value, "partial": bool(part.value)}
+
+
+def demodulate_signal(ctx, x, start_index, lo_freq, cfg):
+    x = np.ascontiguousarray(x, dtype=np.complex64)
+    w = Windows(ctx, x.size, 1, 1)
+    try:
+        _check(lib().tdg_demodulate_signal(ctx.handle, w._h, ctypes.byref(cfg), float(lo_freq), _ptr(x), x.size,
+                                           int(start_index)))
+        return w.get_du(0)
+    finally:
+        w.close()
+
+
+def detection_json_line(rec, tag_id):
+    """detection_json_line (proj/src/recording.cpp:228-242), byte-identical."""
+    r = np.ascontiguousarray(np.atleast_1d(rec).astype(DETECTION_DTYPE))
+    buf = ctypes.create_string_buffer(1024 + 8 * len(tag_id))
+    n = _U64()
+    _check(lib().tdg_detection_json_line(_ptr(r), tag_id.encode(), buf, len(buf), ctypes.byref(n)))
+    return buf.raw[:n.value].decode()

@@ -31,6 +31,30 @@ namespace tdg {
 constexpr int kTileB = 4;   // t2 columns per pass-B tile (M is stored tile-major)
 constexpr int kGroup = 2;   // code pairs per pass-A item (sharing one window spectrum column)
 
+// Build-time layout variants (A/B-timed with tools/ab_libs.sh; the defaults
+// are the measured best):
+//   TDG_NSLOT      operand slots per CTA: 2 = the next item's bulk copies
+//                  overlap this item; 1 = half the shared memory, so more
+//                  CTAs per SM overlap each other instead
+//   TDG_CORR_MINB  CTAs per SM the register budget is sized for
+//   TDG_B_TW_SMEM  pass-B step-2 twiddles from a shared-memory table filled
+//                  once per CTA (instead of chained products)
+//   TDG_B_SEP_TR   pass-B transposes into their own region (one CTA barrier
+//                  per item fewer)
+#ifndef TDG_NSLOT
+#define TDG_NSLOT 2
+#endif
+#ifndef TDG_CORR_MINB
+#define TDG_CORR_MINB 3
+#endif
+#ifndef TDG_B_TW_SMEM
+#define TDG_B_TW_SMEM 0
+#endif
+#ifndef TDG_B_SEP_TR
+#define TDG_B_SEP_TR 0
+#endif
+constexpr int kSlots = TDG_NSLOT;
+
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int qstride_even_pad(int q) { return (q % 2) ? q : q + 1; }
 // pass-B transposed row stride (float2 units): == 4 or 12 (mod 16) so that a
@@ -61,10 +85,13 @@ struct Fused {
     static constexpr int A_OPS = (1 + 2 * kGroup) * XS;
     static constexpr int A_SLOT = up16(A_OPS + 2 * TWS);
     static constexpr int ROWB = passb_row(QB);
-    static constexpr int B_SLOT = up16(cmax(LB * kTileB, PB * ROWB));
+    static constexpr int B_TR = TDG_B_SEP_TR ? up16(PB * ROWB) : 0;        // separate transpose region
+    static constexpr int B_SLOT = TDG_B_SEP_TR ? up16(LB * kTileB) : up16(cmax(LB * kTileB, PB * ROWB));
     static constexpr int SLOT = cmax(A_SLOT, B_SLOT);
+    static constexpr int B_TW = TDG_B_TW_SMEM ? up16(LB) : 0;               // pass-B twiddle table
     static constexpr int NT = 128;
-    static constexpr size_t SMEM = 128 + 2 * size_t(SLOT) * 8;
+    // slots, then (pass B) the transpose region and the twiddle table
+    static constexpr size_t SMEM = 128 + kSlots * size_t(SLOT) * 8 + size_t(B_TR + B_TW) * 8;
     static_assert(cmax(PA, QA) <= 32 && cmax(PB, QB) <= 32, "one warp per column role");
     static_assert(LA % kTileB == 0, "M tiles cover the t2 columns exactly (TMA store box)");
     static_assert(kTileB * cmax(PB, QB) <= NT, "pass-B tasks fit the CTA");
@@ -276,7 +303,8 @@ __device__ __forceinline__ void store_passA(const CorrSched& S, const Desc& D, c
 // proj/src/detector.cpp:122-134) merged with atomicMax on packed keys, or
 // the full xc rows (batch_xcorr diagnostics).
 template <int PA, int QA, int PB, int QB>
-__device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl) {
+__device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl,
+                                           float2* trb, const float2* twb) {
     using F = Fused<PA, QA, PB, QB>;
     constexpr int P = PB, Q = QB, ROW = F::ROWB, TB = kTileB;
     const CorrPairOut& po = D.outs[k.idx / S.n_tiles];
@@ -294,15 +322,16 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
     const int t2l1 = tid % TB, a1 = tid / TB;
     const bool act1 = a1 < P;
     float2 v[Q];
+    float2* tr = TDG_B_SEP_TR ? trb : sl;   // transposed tile: own region, or in place
     if (act1) {
 #pragma unroll
         for (int b = 0; b < Q; ++b) v[b] = sl[(a1 + P * b) * TB + t2l1];
         dft<Q, +1>(v);
     }
-    __syncthreads();
+    if (!TDG_B_SEP_TR) __syncthreads();   // in place: every input read before any transposed write
     if (act1) {
 #pragma unroll
-        for (int c = 0; c < Q; ++c) sl[a1 * ROW + c * TB + t2l1] = v[c];
+        for (int c = 0; c < Q; ++c) tr[a1 * ROW + c * TB + t2l1] = v[c];
     }
     __syncthreads();
     // step 2: task (c, t2l)
@@ -313,8 +342,13 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
     float2 w[P];
     if (c < Q) {
 #pragma unroll
-        for (int a = 0; a < P; ++a) w[a] = sl[a * ROW + c * TB + t2l];
-        apply_step2_twiddles<P, Q>(w, S.twB, c);
+        for (int a = 0; a < P; ++a) w[a] = tr[a * ROW + c * TB + t2l];
+        if (TDG_B_TW_SMEM) {
+#pragma unroll
+            for (int a = 1; a < P; ++a) w[a] = cmul(w[a], twb[a * Q + c]);
+        } else {
+            apply_step2_twiddles<P, Q>(w, S.twB, c);
+        }
         dft<P, +1>(w);
         // valid lags t = t2 + N2*(c + Q*e) < W form a prefix e < e_lim
         if (t2 < N2 && uint32_t(t2) < W) {
@@ -398,11 +432,13 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
 // items with a 2-slot TMA ring (item i+1's bulk copies in flight while item i
 // computes).
 template <int PA, int QA, int PB, int QB, int TYPE>
-__global__ void __launch_bounds__(128, 3) k_corr_pass(const __grid_constant__ CorrSched S) {
+__global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_constant__ CorrSched S) {
     using F = Fused<PA, QA, PB, QB>;
     extern __shared__ __align__(128) unsigned char smraw[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smraw);
     float2* slots = reinterpret_cast<float2*>(smraw + 128);
+    float2* trb = slots + size_t(kSlots) * F::SLOT;   // pass B: separate transpose region (TDG_B_SEP_TR)
+    float2* twb = trb + F::B_TR;                      // pass B: twiddle table (TDG_B_TW_SMEM)
     // the wave's descriptors live in shared memory (read by every item)
     unsigned char* dsm = smraw + F::SMEM;
     const int n_items = TYPE == 0 ? S.nA : S.nB;
@@ -433,24 +469,35 @@ __global__ void __launch_bounds__(128, 3) k_corr_pass(const __grid_constant__ Co
         D.groups = reinterpret_cast<const CorrGroup<kGroup>*>(dsm);
         D.outs = reinterpret_cast<const CorrPairOut*>(dsm + nb_g);
     }
+    if (TYPE == 1 && TDG_B_TW_SMEM)
+        for (int i = threadIdx.x; i < F::LB; i += F::NT) twb[i] = __ldg(&S.twB[i]);
     __syncthreads();
     uint32_t phases = 0u;   // bit s: parity of slot s's mbarrier
-    for (int item = i0, s = 0; item < i1; ++item, s ^= 1) {
-        // next item's bulk copies into slot s^1: pass B at the top of the item;
-        // pass A halfway through (after step 1), once the TMA stores of the
-        // item that last used slot s^1 have read their staging area
+    for (int item = i0, s = 0; item < i1; ++item, s ^= (kSlots - 1)) {
+        // next item's bulk copies into slot s^1 (two slots): pass B at the
+        // top of the item; pass A halfway through (after step 1), once the
+        // TMA stores of the item that last used slot s^1 have read their
+        // staging area.  One slot: after this item (below).
         auto prefetch = [&]() {
-            if (threadIdx.x == 0 && item + 1 < i1) {
+            if (kSlots == 2 && threadIdx.x == 0 && item + 1 < i1) {
                 if (TYPE == 0) bulk_wait_read_all();
                 const Ticket kn{TYPE, 0, item + 1};
                 if (!ticket_noop(S, D, kn))
                     issue_ticket<PA, QA, PB, QB>(S, D, kn, slots + size_t(s ^ 1) * F::SLOT, &bar[s ^ 1]);
             }
         };
+        auto prefetch_after = [&]() {
+            if (kSlots == 1 && threadIdx.x == 0 && item + 1 < i1) {
+                if (TYPE == 0) bulk_wait_read_all();
+                const Ticket kn{TYPE, 0, item + 1};
+                if (!ticket_noop(S, D, kn)) issue_ticket<PA, QA, PB, QB>(S, D, kn, slots, &bar[0]);
+            }
+        };
         if (TYPE == 1) prefetch();
         const Ticket k{TYPE, 0, item};
         if (ticket_noop(S, D, k)) {
             if (TYPE == 0) prefetch();
+            prefetch_after();
             continue;
         }
         float2* sl = slots + size_t(s) * F::SLOT;
@@ -471,10 +518,11 @@ __global__ void __launch_bounds__(128, 3) k_corr_pass(const __grid_constant__ Co
             if (S.discard)
                 for (uintptr_t a = lo + uintptr_t(threadIdx.x) * 128; a < hi; a += uintptr_t(F::NT) * 128)
                     discard_l2(reinterpret_cast<const void*>(a));
-            item_passB<PA, QA, PB, QB>(S, D, k, sl);
+            item_passB<PA, QA, PB, QB>(S, D, k, sl, trb, twb);
         }
         __syncthreads();   // slot s consumed (pass A: its staged columns complete)
         if (TYPE == 0 && threadIdx.x == 0) store_passA<PA, QA, PB, QB>(S, D, k, sl);
+        prefetch_after();
     }
     if (TYPE == 0 && threadIdx.x == 0) bulk_wait_all();
 }

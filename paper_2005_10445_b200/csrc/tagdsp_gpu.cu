@@ -23,6 +23,7 @@
 #include "kernels.cuh"
 #include "corr_v3.cuh"
 #include "peak.cuh"
+#include "generic.cuh"
 #include <cudaTypedefs.h>
 
 namespace {
@@ -514,6 +515,12 @@ struct tdg_ctx {
     int clen = 0;               // composed filter length of the last filter_spectra key
     // scratch
     DevBuf T, M, keys, det_dev, stream_buf, stats_part, stats_ctr;
+    DevBuf gen_a, gen_b, gen_c, gen_d;   // span-level entry points (tdg_fft, tdg_convolve, ...)
+    // detect() stage split (option "detect_timings"): events around the
+    // correlation stage and the statistics of the last detect
+    bool detect_timings = false;
+    cudaEvent_t dt_ev[3] = {nullptr, nullptr, nullptr};
+    double last_corr_s = 0.0, last_stats_s = 0.0;
     // streams + events of the multi-stream correlation pipeline
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::vector<cudaEvent_t> ev_a, ev_b;
@@ -775,6 +782,9 @@ struct tdg_codeset {
     int N1 = 0, N2 = 0;
     uint64_t H = 0;            // half-column spectrum length (N1/2+1)*N2
     uint64_t rep_cap = 0;      // replica_d stride
+    uint64_t cap_codes = 0;    // codes the device buffers hold (grows by doubling on append)
+    uint64_t ref_corr = 0;     // the reference's corr_len (make_transformed precondition)
+    std::vector<double> cfg_key;   // prepared sets: the configuration appended codes must share
     DevBuf spec, rep, nlen_dev, energy_dev, abs_dev;
     std::vector<uint64_t> nlen;
     std::vector<float> energy, abs_sum;
@@ -1172,6 +1182,8 @@ void tdg_ctx_destroy(tdg_ctx* ctx) {
     for (auto x : ctx->a_streams) cudaStreamDestroy(x);
     for (auto x : ctx->b_streams) cudaStreamDestroy(x);
     for (auto e : ctx->ev_fwd) cudaEventDestroy(e);
+    for (auto e : ctx->dt_ev)
+        if (e) cudaEventDestroy(e);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -1241,6 +1253,8 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
             ctx->track_graphs_on = value != 0;
         else if (k == "fwd_wave")
             ctx->fwd_wave = value > 0 ? value : 32;
+        else if (k == "detect_timings")
+            ctx->detect_timings = value != 0;
         else
             fail(TDG_EINVAL, "unknown option %s", key);
     });
@@ -1249,50 +1263,99 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
 // ---- code sets -------------------------------------------------------------
 namespace {
 
-void finish_codeset(tdg_ctx* ctx, tdg_codeset* cs, const float* d, const float* u, uint64_t stride,
-                    const std::vector<uint64_t>& lens, uint64_t ref_corr_len) {
-    const uint64_t n = cs->n_codes;
-    cs->nlen_dev.ensure(n * sizeof(uint64_t));
-    cs->energy_dev.ensure(n * sizeof(float));
-    cs->abs_dev.ensure(n * sizeof(float));
-    cs->rep_cap = 0;
-    for (uint64_t l : lens) cs->rep_cap = std::max(cs->rep_cap, l);
-    cs->rep_cap = (std::max<uint64_t>(cs->rep_cap, 1) + 3) & ~uint64_t(3);   // 16-byte rows (stats vector loads)
-    cs->rep.ensure(n * cs->rep_cap * sizeof(float));
+// grow a device buffer to `bytes`, keeping its first `keep` bytes
+void grow_keep(tdg_ctx* ctx, DevBuf& buf, size_t bytes, size_t keep) {
+    if (bytes <= buf.bytes) return;
+    DevBuf nb;
+    nb.ensure(bytes);
+    if (keep) CK(cudaMemcpyAsync(nb.p, buf.p, keep, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    std::swap(nb.p, buf.p);
+    std::swap(nb.bytes, buf.bytes);
+}
+
+// Append n codes to cs from their demodulated replicas (d, u at `stride`,
+// lens[i] samples each): support n, energy and abs_sum (make_transformed,
+// proj/src/detector.cpp:20-43), then the forward transforms of every stored
+// pair the new codes touch -- or of all pairs if the longer support needs a
+// longer transform.  Device buffers grow by doubling, so a roster built one
+// prepare_code at a time costs O(C) transforms, not O(C^2).
+void append_codes(tdg_ctx* ctx, tdg_codeset* cs, const float* d, const float* u, uint64_t stride,
+                  const std::vector<uint64_t>& lens, uint64_t ref_corr_len) {
+    const uint64_t n0 = cs->n_codes, n = lens.size(), nt = n0 + n;
+    uint64_t rc = 0;
+    for (uint64_t l : lens) rc = std::max(rc, l);
+    rc = (std::max<uint64_t>(rc, 1) + 3) & ~uint64_t(3);   // 16-byte rows (stats vector loads)
+    if (n0 && rc > cs->rep_cap) fail(TDG_EINVAL, "prepare_code: replica longer than the code set's stride");
+    if (!n0) cs->rep_cap = rc;
+    if (nt > cs->cap_codes) {
+        const uint64_t cap = std::max<uint64_t>(nt, n0 ? 2 * cs->cap_codes : nt);
+        grow_keep(ctx, cs->rep, cap * cs->rep_cap * sizeof(float), n0 * cs->rep_cap * sizeof(float));
+        grow_keep(ctx, cs->nlen_dev, cap * sizeof(uint64_t), n0 * sizeof(uint64_t));
+        grow_keep(ctx, cs->energy_dev, cap * sizeof(float), n0 * sizeof(float));
+        grow_keep(ctx, cs->abs_dev, cap * sizeof(float), n0 * sizeof(float));
+        cs->cap_codes = cap;
+    }
     std::vector<tdg::SupportDesc> sd(n);
-    for (uint64_t i = 0; i < n; ++i)
-        sd[i] = {d + i * stride, u ? u + i * stride : nullptr, lens[i], cs->rep.as<float>() + i * cs->rep_cap,
-                 cs->rep_cap, cs->nlen_dev.as<uint64_t>() + i, cs->energy_dev.as<float>() + i, cs->abs_dev.as<float>() + i};
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint64_t c = n0 + i;
+        sd[i] = {d + i * stride, u ? u + i * stride : nullptr, lens[i], cs->rep.as<float>() + c * cs->rep_cap,
+                 cs->rep_cap, cs->nlen_dev.as<uint64_t>() + c, cs->energy_dev.as<float>() + c,
+                 cs->abs_dev.as<float>() + c};
+    }
     auto* sdd = ctx->upload(ctx->pk->stats, sd);
     tdg::k_support<<<unsigned(n), 1024, 0, ctx->stream>>>(sdd);
     LAUNCHED();
-    cs->nlen.resize(n);
-    cs->energy.resize(n);
-    cs->abs_sum.resize(n);
-    CK(cudaMemcpyAsync(cs->nlen.data(), cs->nlen_dev.p, n * sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(cs->energy.data(), cs->energy_dev.p, n * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(cs->abs_sum.data(), cs->abs_dev.p, n * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+    cs->nlen.resize(nt);
+    cs->energy.resize(nt);
+    cs->abs_sum.resize(nt);
+    CK(cudaMemcpyAsync(cs->nlen.data() + n0, cs->nlen_dev.as<uint64_t>() + n0, n * sizeof(uint64_t),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(cs->energy.data() + n0, cs->energy_dev.as<float>() + n0, n * sizeof(float),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(cs->abs_sum.data() + n0, cs->abs_dev.as<float>() + n0, n * sizeof(float),
+                       cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     uint64_t nmax = 1;
-    for (uint64_t i = 0; i < n; ++i) {
+    for (uint64_t i = 0; i < nt; ++i) {
         // make_transformed precondition (proj/src/detector.cpp:28-29)
-        if (cs->window_len + cs->nlen[i] > ref_corr_len + 1)
+        if (i >= n0 && cs->window_len + cs->nlen[i] > ref_corr_len + 1) {
+            cs->nlen.resize(n0);
+            cs->energy.resize(n0);
+            cs->abs_sum.resize(n0);
             fail(TDG_EINVAL, "make_transformed: transform too short for linear correlation");
+        }
         nmax = std::max(nmax, cs->nlen[i]);
     }
     if (cs->window_len >= (uint64_t(1) << 32)) fail(TDG_ERANGE, "window_len too large");
-    if (!choose_corr_len(cs->window_len + nmax - 1, &cs->N1, &cs->N2))
+    int N1 = 0, N2 = 0;
+    if (!choose_corr_len(cs->window_len + nmax - 1, &N1, &N2)) {
+        cs->nlen.resize(n0);
+        cs->energy.resize(n0);
+        cs->abs_sum.resize(n0);
         fail(TDG_ERANGE, "window_len + support %llu exceeds the largest supported transform",
              (unsigned long long)(cs->window_len + nmax));
-    cs->H = uint64_t(cs->N1 / 2 + 1) * uint64_t(cs->N2);
+    }
+    cs->n_codes = nt;
+    const bool relen = N1 != cs->N1 || N2 != cs->N2;
+    cs->N1 = N1;
+    cs->N2 = N2;
+    cs->H = uint64_t(N1 / 2 + 1) * uint64_t(N2);
     const uint64_t N = cs->corr_len();
-    const uint64_t npairs = (n + 1) / 2;
-    cs->spec.ensure(npairs * N * sizeof(float2));
+    const uint64_t npairs = (nt + 1) / 2, pcap = (cs->cap_codes + 1) / 2;
+    const uint64_t first_pair = relen ? 0 : n0 / 2;
+    if (relen) {
+        cs->spec.release();
+        cs->spec.ensure(pcap * N * sizeof(float2));
+    } else {
+        grow_keep(ctx, cs->spec, pcap * N * sizeof(float2), first_pair * N * sizeof(float2));
+    }
     std::vector<FwdJob> jobs;
-    for (uint64_t i = 0; i < n; i += 2) {
-        const bool two = i + 1 < n;
+    for (uint64_t p = first_pair; p < npairs; ++p) {
+        const uint64_t i = 2 * p;
+        const bool two = i + 1 < nt;
         jobs.push_back({cs->rep.as<float>() + i * cs->rep_cap, two ? cs->rep.as<float>() + (i + 1) * cs->rep_cap : nullptr,
-                        cs->nlen[i], two ? cs->nlen[i + 1] : 0, cs->spec.as<float2>() + (i / 2) * N, nullptr});
+                        cs->nlen[i], two ? cs->nlen[i + 1] : 0, cs->spec.as<float2>() + p * N, nullptr});
     }
     run_forward(ctx, cs->N1, cs->N2, jobs, false);
     CK(cudaStreamSynchronize(ctx->stream));
@@ -1332,47 +1395,75 @@ void demod_launch(tdg_ctx* ctx, const void* in, bool int16_input, uint64_t in_le
 
 }  // namespace
 
+namespace {
+std::vector<double> cfg_key_of(const tdg_demod_config& c) {
+    return {c.mod.sample_rate, c.mod.bit_rate, c.mod.freq_one, c.mod.freq_zero, double(c.mod.packet_bits),
+            c.bandpass_center, c.bandpass_width, double(c.bandpass_taps), double(c.eps)};
+}
+
+// prepare_code (proj/src/detector.cpp:50-66) for n codes, appended to cs:
+// synth_replica -> demodulation with lo_freq = 0 -> support / energy ->
+// forward transforms of the touched pairs, all on the GPU
+void prepare_codes(tdg_ctx* ctx, tdg_codeset* cs, const tdg_demod_config& c, const uint8_t* bits, uint64_t n_codes) {
+    validate_cfg(c);
+    const uint64_t spb = samples_per_bit(c.mod);
+    const uint64_t nbits = c.mod.packet_bits;
+    const uint64_t psamp = nbits * spb;
+    const uint64_t window_len = cs->window_len;
+    if (window_len < psamp) fail(TDG_EINVAL, "prepare_code: window shorter than a packet");
+    if (n_codes == 0) fail(TDG_EINVAL, "prepare_code: no codes");
+    const std::vector<double> key = cfg_key_of(c);
+    if (cs->n_codes && cs->cfg_key != key)
+        fail(TDG_EINVAL, "prepare_code: the code set was prepared with another configuration");
+    cs->cfg_key = key;
+    const uint64_t clen_ref = c.bandpass_taps + spb - 1;
+    cs->ref_corr = pad_length_impl(window_len + psamp + clen_ref);
+    // filters for lo = 0 (replicas skip the local oscillator, proj/src/detector.cpp:59-61)
+    const float2* H = ctx->filter_spectra(c, std::vector<double>{0.0});
+    // replica demod span: the packet plus the filter tail plus one block of margin
+    const uint64_t Wr = std::min<uint64_t>(window_len, psamp + uint64_t(ctx->clen) + 1024);
+    DevBuf dbits, drep, dd, du;
+    dbits.ensure(n_codes * nbits);
+    CK(cudaMemcpyAsync(dbits.p, bits, n_codes * nbits, cudaMemcpyHostToDevice, ctx->stream));
+    drep.ensure(n_codes * Wr * sizeof(float2));
+    const double pi = 3.14159265358979323846;
+    const double step1 = 2.0 * pi * c.mod.freq_one / c.mod.sample_rate;
+    const double step0 = 2.0 * pi * c.mod.freq_zero / c.mod.sample_rate;
+    tdg::k_synth_replica<<<unsigned(n_codes), 1024, nbits * sizeof(uint32_t), ctx->stream>>>(
+        dbits.as<uint8_t>(), uint32_t(nbits), uint32_t(spb), step1, step0, drep.as<float2>(), Wr);
+    LAUNCHED();
+    dd.ensure(n_codes * Wr * sizeof(float));
+    du.ensure(n_codes * Wr * sizeof(float));
+    std::vector<tdg::DemodWindowDesc> wins(n_codes);
+    for (uint64_t i = 0; i < n_codes; ++i) wins[i] = {i * Wr, dd.as<float>() + i * Wr, du.as<float>() + i * Wr};
+    demod_launch(ctx, drep.p, false, n_codes * Wr, wins, Wr, 1, Wr, H, c.eps);
+    std::vector<uint64_t> lens(n_codes, Wr);
+    append_codes(ctx, cs, dd.as<float>(), du.as<float>(), Wr, lens, cs->ref_corr);
+}
+}  // namespace
+
 int tdg_codeset_prepare(tdg_ctx* ctx, const tdg_demod_config* cfg, uint64_t window_len, const uint8_t* bits,
                         uint64_t n_codes, tdg_codeset** out) {
     return guard([&] {
         *out = nullptr;
         CK(cudaSetDevice(ctx->device));
-        const tdg_demod_config& c = *cfg;
-        validate_cfg(c);
-        const uint64_t spb = samples_per_bit(c.mod);
-        const uint64_t nbits = c.mod.packet_bits;
-        const uint64_t psamp = nbits * spb;
-        if (window_len < psamp) fail(TDG_EINVAL, "prepare_code: window shorter than a packet");
-        if (n_codes == 0) fail(TDG_EINVAL, "prepare_code: no codes");
-        const uint64_t clen_ref = c.bandpass_taps + spb - 1;
-        const uint64_t ref_corr = pad_length_impl(window_len + psamp + clen_ref);
-        // filters for lo = 0 (replicas skip the local oscillator, proj/src/detector.cpp:59-61)
-        const float2* H = ctx->filter_spectra(c, std::vector<double>{0.0});
-        // replica demod span: the packet plus the filter tail plus one block of margin
-        const uint64_t Wr = std::min<uint64_t>(window_len, psamp + uint64_t(ctx->clen) + 1024);
         auto cs = std::make_unique<tdg_codeset>();
         cs->ctx = ctx;
         cs->device = ctx->device;
         cs->window_len = window_len;
-        cs->n_codes = n_codes;
-        DevBuf dbits, drep, dd, du;
-        dbits.ensure(n_codes * nbits);
-        CK(cudaMemcpyAsync(dbits.p, bits, n_codes * nbits, cudaMemcpyHostToDevice, ctx->stream));
-        drep.ensure(n_codes * Wr * sizeof(float2));
-        const double pi = 3.14159265358979323846;
-        const double step1 = 2.0 * pi * c.mod.freq_one / c.mod.sample_rate;
-        const double step0 = 2.0 * pi * c.mod.freq_zero / c.mod.sample_rate;
-        tdg::k_synth_replica<<<unsigned(n_codes), 1024, nbits * sizeof(uint32_t), ctx->stream>>>(
-            dbits.as<uint8_t>(), uint32_t(nbits), uint32_t(spb), step1, step0, drep.as<float2>(), Wr);
-        LAUNCHED();
-        dd.ensure(n_codes * Wr * sizeof(float));
-        du.ensure(n_codes * Wr * sizeof(float));
-        std::vector<tdg::DemodWindowDesc> wins(n_codes);
-        for (uint64_t i = 0; i < n_codes; ++i) wins[i] = {i * Wr, dd.as<float>() + i * Wr, du.as<float>() + i * Wr};
-        demod_launch(ctx, drep.p, false, n_codes * Wr, wins, Wr, 1, Wr, H, c.eps);
-        std::vector<uint64_t> lens(n_codes, Wr);
-        finish_codeset(ctx, cs.get(), dd.as<float>(), du.as<float>(), Wr, lens, ref_corr);
+        prepare_codes(ctx, cs.get(), *cfg, bits, n_codes);
         *out = cs.release();
+    });
+}
+
+int tdg_codeset_append(tdg_ctx* ctx, tdg_codeset* cs, const tdg_demod_config* cfg, const uint8_t* bits,
+                       uint64_t n_codes) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (cs->device != ctx->device) fail(TDG_EINVAL, "prepare_code: code set on another device");
+        if (cs->n_codes && cs->cfg_key.empty())
+            fail(TDG_EINVAL, "prepare_code: cannot append prepared codes to a make_transformed code set");
+        prepare_codes(ctx, cs, *cfg, bits, n_codes);
     });
 }
 
@@ -1399,7 +1490,7 @@ int tdg_codeset_from_replicas(tdg_ctx* ctx, uint64_t window_len, uint64_t corr_l
         cs->ctx = ctx;
         cs->device = ctx->device;
         cs->window_len = window_len;
-        cs->n_codes = n_codes;
+        cs->ref_corr = corr_len;
         DevBuf dd, du;
         dd.ensure(hd.size() * sizeof(float));
         CK(cudaMemcpyAsync(dd.p, hd.data(), hd.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
@@ -1407,7 +1498,7 @@ int tdg_codeset_from_replicas(tdg_ctx* ctx, uint64_t window_len, uint64_t corr_l
             du.ensure(hu.size() * sizeof(float));
             CK(cudaMemcpyAsync(du.p, hu.data(), hu.size() * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
         }
-        finish_codeset(ctx, cs.get(), dd.as<float>(), have_u ? du.as<float>() : nullptr, stride, lens, corr_len);
+        append_codes(ctx, cs.get(), dd.as<float>(), have_u ? du.as<float>() : nullptr, stride, lens, corr_len);
         *out = cs.release();
     });
 }
@@ -1541,6 +1632,14 @@ int tdg_windows_set_du(tdg_ctx* ctx, tdg_windows* w, uint64_t slot, const float*
     });
 }
 
+int tdg_windows_set_start(tdg_ctx* ctx, tdg_windows* w, uint64_t slot, int64_t window_start) {
+    return guard([&] {
+        (void)ctx;
+        if (slot >= w->slots()) fail(TDG_EINVAL, "slot out of range");
+        w->start[slot] = window_start;
+    });
+}
+
 int tdg_windows_get_du(tdg_ctx* ctx, const tdg_windows* w, uint64_t slot, float* d, float* u) {
     return guard([&] {
         CK(cudaSetDevice(ctx->device));
@@ -1616,19 +1715,38 @@ void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float thre
             x.bin = int32_t(s % w->n_bins);
         }
     auto* sdd = ctx->upload(ctx->pk->stats, sd);
+    const bool timed = ctx->detect_timings && !tl_graph_mode;
+    if (timed) {
+        for (auto& e : ctx->dt_ev)
+            if (!e) CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(ctx->dt_ev[0], ctx->stream));
+    }
     {
         // correlation stage incl. the forward transforms it overlaps (those are
         // also timed on their own as fwd_pass1/2)
         KScope ks(ctx, "corr");
         run_correlations(ctx, w, cs, jobs, false);
     }
+    if (timed) CK(cudaEventRecord(ctx->dt_ev[1], ctx->stream));
     // (running each finished code group's statistics under later waves on the
     // second stream was measured slower: it delays the pass-B launches queued
     // behind it and takes SM slots from the persistent passes)
     launch_stats(ctx, sdd, sd.size(), uint32_t(w->W), fs, threshold);
+    if (timed) CK(cudaEventRecord(ctx->dt_ev[2], ctx->stream));
     if (out) {
         CK(cudaMemcpyAsync(out, ctx->det_dev.p, ns * nk * sizeof(tdg_detection), cudaMemcpyDeviceToHost, ctx->stream));
         if (sync) CK(cudaStreamSynchronize(ctx->stream));
+    }
+    if (timed) {
+        // DetectTimings (detector.hpp:95-98): correlation = forward transform +
+        // spectral products + inverse transforms + argmax; peak_stats = refinement
+        // and statistics
+        CK(cudaEventSynchronize(ctx->dt_ev[2]));
+        float a = 0.f, b = 0.f;
+        CK(cudaEventElapsedTime(&a, ctx->dt_ev[0], ctx->dt_ev[1]));
+        CK(cudaEventElapsedTime(&b, ctx->dt_ev[1], ctx->dt_ev[2]));
+        ctx->last_corr_s = a * 1e-3;
+        ctx->last_stats_s = b * 1e-3;
     }
 }
 }  // namespace
@@ -2131,6 +2249,219 @@ int tdg_fp32_peak(int device, double* ffma_tflops, double* ffma2_tflops) {
         cudaStreamDestroy(st);
         if (ffma_tflops) *ffma_tflops = best1;
         if (ffma2_tflops) *ffma2_tflops = best2;
+    });
+}
+
+// ---------------------------------------------------------------------------
+// Span-level entry points: the reference functions that take and return host
+// arrays (the drop-in's fft.hpp / dsp.hpp / detector.hpp surface), each one a
+// device round trip through the kernels of generic.cuh / kernels.cuh.
+namespace {
+int grid_for(uint64_t n) { return int(std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, uint64_t(num_sms()) * 16))); }
+
+// {2,3,5,7}-smooth radix plan, largest radices first (8 and 4 for powers of two)
+std::vector<int> radix_plan(uint64_t n) {
+    std::vector<int> r;
+    uint64_t m = n;
+    while (m % 8 == 0) { r.push_back(8); m /= 8; }
+    while (m % 4 == 0) { r.push_back(4); m /= 4; }
+    while (m % 2 == 0) { r.push_back(2); m /= 2; }
+    for (int p : {7, 5, 3})
+        while (m % uint64_t(p) == 0) { r.push_back(p); m /= uint64_t(p); }
+    if (m != 1) fail(TDG_ERANGE, "fft: length %llu is not {2,3,5,7}-smooth", (unsigned long long)n);
+    return r;
+}
+
+// in-place-by-ping-pong Stockham FFT of the n complex values at a; the result
+// is in a (copied back if the stage count is odd).  inverse: sign +1 and 1/n.
+void fft_device(tdg_ctx* ctx, float2* a, float2* tmp, uint64_t n, bool inverse) {
+    if (n >= (uint64_t(1) << 32)) fail(TDG_ERANGE, "fft: length too large");
+    const auto plan = radix_plan(n);
+    float2 *src = a, *dst = tmp;
+    uint32_t ns = 1;
+    for (size_t s = 0; s < plan.size(); ++s) {
+        const float scale = (inverse && s + 1 == plan.size()) ? float(1.0 / double(n)) : 1.0f;
+        const int R = plan[s];
+        const int g = grid_for(n / uint64_t(R));
+#define STAGE(RR)                                                                                              \
+    if (R == RR) {                                                                                             \
+        if (inverse) tdg::k_stockham<RR, 1><<<g, 256, 0, ctx->stream>>>(src, dst, uint32_t(n), ns, scale);     \
+        else tdg::k_stockham<RR, -1><<<g, 256, 0, ctx->stream>>>(src, dst, uint32_t(n), ns, scale);            \
+    }
+        STAGE(2) STAGE(3) STAGE(4) STAGE(5) STAGE(7) STAGE(8)
+#undef STAGE
+        LAUNCHED();
+        ns *= uint32_t(R);
+        std::swap(src, dst);
+    }
+    if (src != a) CK(cudaMemcpyAsync(a, src, n * sizeof(float2), cudaMemcpyDeviceToDevice, ctx->stream));
+}
+}  // namespace
+
+int tdg_fft(tdg_ctx* ctx, const float* in, float* out, uint64_t n, int inverse) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (n == 0) fail(TDG_EINVAL, "fft: empty transform");
+        ctx->gen_a.ensure(n * sizeof(float2));
+        ctx->gen_b.ensure(n * sizeof(float2));
+        CK(cudaMemcpyAsync(ctx->gen_a.p, in, n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+        fft_device(ctx, ctx->gen_a.as<float2>(), ctx->gen_b.as<float2>(), n, inverse != 0);
+        CK(cudaMemcpyAsync(out, ctx->gen_a.p, n * sizeof(float2), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int tdg_convert(tdg_ctx* ctx, const int16_t* iq, uint64_t n_int16, float* out) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (n_int16 % 2) fail(TDG_EINVAL, "convert: odd raw sample count");
+        const uint64_t n = n_int16 / 2;
+        if (!n) return;
+        ctx->gen_c.ensure(n * 2 * sizeof(int16_t));
+        ctx->gen_a.ensure(n * sizeof(float2));
+        CK(cudaMemcpyAsync(ctx->gen_c.p, iq, n * 2 * sizeof(int16_t), cudaMemcpyHostToDevice, ctx->stream));
+        tdg::k_convert<<<grid_for(n), 256, 0, ctx->stream>>>(ctx->gen_c.as<short2>(), ctx->gen_a.as<float2>(), n);
+        LAUNCHED();
+        CK(cudaMemcpyAsync(out, ctx->gen_a.p, n * sizeof(float2), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int tdg_mix(tdg_ctx* ctx, float* x, uint64_t n, double lo_freq, int64_t start_index, double sample_rate) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (lo_freq == 0.0 || n == 0) return;   // the reference's no-op (dsp.cpp:19)
+        ctx->gen_a.ensure(n * sizeof(float2));
+        CK(cudaMemcpyAsync(ctx->gen_a.p, x, n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+        tdg::k_mix<<<grid_for(n), 256, 0, ctx->stream>>>(ctx->gen_a.as<float2>(), n, lo_freq / sample_rate, start_index);
+        LAUNCHED();
+        CK(cudaMemcpyAsync(x, ctx->gen_a.p, n * sizeof(float2), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int tdg_convolve(tdg_ctx* ctx, const float* x, uint64_t nx, const float* h, uint64_t nh, float* out) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (nh == 0) fail(TDG_EINVAL, "overlap_add_filter: empty filter");
+        if (nx == 0) return;
+        const uint64_t nf = nx + nh - 1, L = pad_length_impl(nf);
+        ctx->gen_a.ensure(L * sizeof(float2));
+        ctx->gen_b.ensure(L * sizeof(float2));
+        ctx->gen_d.ensure(L * sizeof(float2));
+        float2* A = ctx->gen_a.as<float2>();
+        float2* B = ctx->gen_d.as<float2>();
+        CK(cudaMemsetAsync(A, 0, L * sizeof(float2), ctx->stream));
+        CK(cudaMemsetAsync(B, 0, L * sizeof(float2), ctx->stream));
+        CK(cudaMemcpyAsync(A, x, nx * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(B, h, nh * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+        fft_device(ctx, A, ctx->gen_b.as<float2>(), L, false);
+        fft_device(ctx, B, ctx->gen_b.as<float2>(), L, false);
+        tdg::k_cmul_inplace<<<grid_for(L), 256, 0, ctx->stream>>>(A, B, L);
+        LAUNCHED();
+        fft_device(ctx, A, ctx->gen_b.as<float2>(), L, true);
+        CK(cudaMemcpyAsync(out, A, nf * sizeof(float2), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int tdg_discriminate(tdg_ctx* ctx, const float* f1, const float* f0, uint64_t n, float eps, float* d, float* u) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (!n) return;
+        ctx->gen_a.ensure(n * sizeof(float2));
+        ctx->gen_b.ensure(n * sizeof(float2));
+        ctx->gen_c.ensure(2 * n * sizeof(float));
+        CK(cudaMemcpyAsync(ctx->gen_a.p, f1, n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->gen_b.p, f0, n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+        float* dd = ctx->gen_c.as<float>();
+        tdg::k_discriminate<<<grid_for(n), 256, 0, ctx->stream>>>(ctx->gen_a.as<float2>(), ctx->gen_b.as<float2>(), n, eps,
+                                                                  dd, dd + n);
+        LAUNCHED();
+        CK(cudaMemcpyAsync(d, dd, n * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(u, dd + n, n * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int tdg_find_peak(tdg_ctx* ctx, const float* xc, uint64_t n, uint64_t* j, float* value) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (n == 0) fail(TDG_EINVAL, "find_peak: empty correlation");
+        if (n >= (uint64_t(1) << 32)) fail(TDG_ERANGE, "find_peak: length too large");
+        ctx->gen_c.ensure(n * sizeof(float));
+        ctx->gen_d.ensure(sizeof(unsigned long long));
+        CK(cudaMemcpyAsync(ctx->gen_c.p, xc, n * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemsetAsync(ctx->gen_d.p, 0, sizeof(unsigned long long), ctx->stream));
+        tdg::k_argmax_abs<<<grid_for(n), 256, 0, ctx->stream>>>(ctx->gen_c.as<float>(), n,
+                                                                ctx->gen_d.as<unsigned long long>());
+        LAUNCHED();
+        unsigned long long key = 0;
+        CK(cudaMemcpyAsync(&key, ctx->gen_d.p, sizeof(key), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        const uint64_t jj = 0xFFFFFFFFull - (key & 0xFFFFFFFFull);
+        *j = jj;
+        *value = xc[jj];   // the signed value at the peak (detector.cpp:133)
+    });
+}
+
+int tdg_statistics(tdg_ctx* ctx, const float* d, const float* u, uint64_t W, const float* dc, uint64_t n, uint64_t j,
+                   float* w_c, float* q, float* p_c, int* partial) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (W >= (uint64_t(1) << 32) || n >= (uint64_t(1) << 32)) fail(TDG_ERANGE, "statistics: length too large");
+        const uint64_t ncap = (std::max<uint64_t>(n, 1) + 3) & ~uint64_t(3);
+        ctx->gen_c.ensure((2 * W + ncap + 8) * sizeof(float));
+        ctx->gen_d.ensure(sizeof(unsigned long long) + sizeof(tdg_detection) + sizeof(tdg::StatsDesc) + 64);
+        float* dd = ctx->gen_c.as<float>();
+        float* uu = dd + W;
+        // 16-byte aligned replica (the statistics kernel's vector path)
+        float* cc = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(uu + W) + 15) & ~uintptr_t(15));
+        CK(cudaMemsetAsync(cc, 0, ncap * sizeof(float), ctx->stream));
+        CK(cudaMemcpyAsync(dd, d, W * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(uu, u, W * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        if (n) CK(cudaMemcpyAsync(cc, dc, n * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+        char* base = static_cast<char*>(ctx->gen_d.p);
+        auto* key = reinterpret_cast<unsigned long long*>(base);
+        auto* det = reinterpret_cast<tdg_detection*>(base + 64);
+        auto* desc = reinterpret_cast<tdg::StatsDesc*>(base + 64 + ((sizeof(tdg_detection) + 63) & ~size_t(63)));
+        const unsigned long long k = 0xFFFFFFFFull - (j & 0xFFFFFFFFull);   // peak_key(0, j)
+        tdg::StatsDesc sd{dd, uu, cc, key, det, uint32_t(n), 1.0f, 0, 0, 0};
+        CK(cudaMemcpyAsync(key, &k, sizeof(k), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(desc, &sd, sizeof(sd), cudaMemcpyHostToDevice, ctx->stream));
+        tdg::k_stats<false><<<1, 256, 0, ctx->stream>>>(desc, uint32_t(W), 1.0, 0.25f, 1, nullptr, nullptr);
+        LAUNCHED();
+        tdg_detection r;
+        CK(cudaMemcpyAsync(&r, det, sizeof(r), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        *w_c = r.w_c;
+        *q = r.q;
+        *p_c = r.p_c;
+        *partial = r.partial;
+    });
+}
+
+int tdg_demodulate_signal(tdg_ctx* ctx, tdg_windows* win, const tdg_demod_config* cfg, double lo_freq, const float* x,
+                          uint64_t n, int64_t start_index) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        if (win->W != n || win->slots() < 1) fail(TDG_EINVAL, "demodulate_signal: window set shape");
+        std::vector<double> bins{lo_freq};
+        const float2* H = ctx->filter_spectra(*cfg, bins);
+        ctx->gen_a.ensure(std::max<uint64_t>(n, 1) * sizeof(float2));
+        CK(cudaMemcpyAsync(ctx->gen_a.p, x, n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+        std::vector<tdg::DemodWindowDesc> wins{{0, win->d.as<float>(), win->u.as<float>()}};
+        demod_launch(ctx, ctx->gen_a.p, false, n, wins, n, 1, n, H, cfg->eps);
+        win->start[0] = start_index;
+        win->dspec_N = 0;
+        CK(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int tdg_detect_timings(tdg_ctx* ctx, double* correlation_s, double* peak_stats_s) {
+    return guard([&] {
+        if (correlation_s) *correlation_s = ctx->last_corr_s;
+        if (peak_stats_s) *peak_stats_s = ctx->last_stats_s;
     });
 }
 

@@ -35,7 +35,7 @@ def write_recording(payload_path, iq, sample_rate, start_time=0, center_freq=0.0
     meta = {"sample_rate": float(sample_rate), "start_time": int(start_time), "center_freq": float(center_freq),
             "creator": creator}
     with open(sidecar_path(payload_path), "w") as f:
-        f.write(json.dumps(meta, indent=2, sort_keys=True) + "\n")
+        f.write(json.dumps(meta, indent=2, sort_keys=True, ensure_ascii=False) + "\n")
 
 
 def read_recording(payload_path):
@@ -59,13 +59,9 @@ def read_recording(payload_path):
 
 
 def detection_json_line(rec, tag_id):
-    """recording.cpp:228-242 (nlohmann dump: sorted keys, no spaces)."""
-    return json.dumps({"tag_id": tag_id, "toa_seconds": float(rec["toa_seconds"]),
-                       "peak_index": int(rec["peak_index"]),
-                       "subsample_offset": float(rec["subsample_offset"]), "w_c": float(rec["w_c"]),
-                       "q": float(rec["q"]), "p_c": float(rec["p_c"]), "score": float(rec["score"]),
-                       "accepted": bool(rec["accepted"]), "partial": bool(rec["partial"])},
-                      sort_keys=True, separators=(",", ":"))
+    """recording.cpp:228-242, through the library (the reference's own
+    nlohmann dump: byte-identical number formatting and escaping)."""
+    return capi.detection_json_line(rec, tag_id)
 
 
 def detect_recording(ctx, payload_path, tags, window_s=0.100, overlap_s=0.010, threshold=0.25, cfg=None,

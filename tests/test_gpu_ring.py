@@ -1,6 +1,6 @@
 """Device-resident CircularBuffer (tdg_ring_*) on the GPU: push / read / gap /
-eviction semantics against a line-by-line Python restatement of the
-reference's CircularBuffer (proj/src/scheduler.cpp:7-45), and searches /
+eviction semantics against the reference's CircularBuffer compiled in place
+(oracle/_ref, proj/src/scheduler.cpp:7-45), and searches /
 tracking tasks that read their windows from the ring against the same passes
 over a linear block (identical kernels, so identical records)."""
 import numpy as np
@@ -10,44 +10,32 @@ pytestmark = pytest.mark.gpu
 
 
 class RefRing:
-    """proj/src/scheduler.cpp:7-45, restated (test oracle)."""
+    """The reference's CircularBuffer compiled in place (oracle/_ref,
+    proj/src/scheduler.cpp:7-45) behind the interface the test uses."""
 
-    def __init__(self, cap):
-        self.cap = cap
-        self.store = np.zeros(2 * cap, np.int16)
-        self.head = self.tail = 0
+    def __init__(self, ref, cap):
+        self.r = ref.Ring(cap)
 
     def push(self, iq, start):
-        gap, eb, ee = False, 0, 0
-        if start != self.tail:                                   # :13-19
-            gap, eb, ee = True, self.head, self.tail
-            self.head = self.tail = start
-        n = iq.size // 2
-        for i in range(n):                                       # :20-24
-            slot = (self.tail + i) % self.cap
-            self.store[2 * slot:2 * slot + 2] = iq[2 * i:2 * i + 2]
-        self.tail += n
-        if self.tail - self.head > self.cap:                     # :26-32
-            if not gap:
-                eb, ee = self.head, self.tail - self.cap
-            self.head = self.tail - self.cap
-        return eb, ee, gap
+        return self.r.push(iq, start)
 
     def read(self, start, end):
-        if start < self.head or end > self.tail or start > end:  # :36
-            return None
-        out = np.empty(2 * (end - start), np.int16)
-        for t in range(start, end):
-            slot = t % self.cap
-            out[2 * (t - start):2 * (t - start) + 2] = self.store[2 * slot:2 * slot + 2]
-        return out
+        return self.r.read(start, end)
+
+    @property
+    def head(self):
+        return self.r.bounds()[0]
+
+    @property
+    def tail(self):
+        return self.r.bounds()[1]
 
 
-def test_ring_semantics_match_reference(gpu_ctx):
+def test_ring_semantics_match_reference(gpu_ctx, ref):
     from paper_2005_10445_b200 import capi
     rng = np.random.default_rng(3)
     cap = 1000
-    ring, ref = capi.Ring(gpu_ctx, cap), RefRing(cap)
+    ring, ref = capi.Ring(gpu_ctx, cap), RefRing(ref, cap)
     t = 0
     # contiguous pushes (wrap-around and eviction), a gap, a block larger than
     # the capacity, an empty block

@@ -11,7 +11,7 @@ python tools/sweep.py "" "" "" "" > /dev/null 2>&1   # warm the GPU
 for i in 1 2 3; do
   for v in $VARIANTS; do
     case $MODE in
-    detect) TDG_LIB_PATH=abtest/lib_$v.so python tools/sweep.py "" "" "" | tail -2 | sed "s/^/$v /" >> "$OUT/ab.txt" ;;
+    detect) TDG_LIB_PATH=abtest/lib_$v.so python tools/sweep.py "" ${SPECS:-"" ""} | tail -n +2 | sed "s/^/$v /" >> "$OUT/ab.txt" ;;
     step) TDG_LIB_PATH=abtest/lib_$v.so python bench.py --no-cpu-baseline --steps 20 2>/dev/null | python -c "
 import json,sys; d=json.loads(sys.stdin.read()); print('$v value %.0f e2e %.0f' % (d['value'], d['e2e']['value']))" >> "$OUT/ab.txt" ;;
     track) TDG_LIB_PATH=abtest/lib_$v.so python bench.py --workload tracking 2>/dev/null | python -c "

@@ -49,7 +49,7 @@ def main():
         ctx.synchronize()
         ms = e0.elapsed_time(e1) / reps
         out = (ctypes.c_char * (n_units * 64))()
-        capi._check(lib.tdg_detect(ctx.handle, win._h, cs._h, 0.25, bench.FS, out, out.size))
+        capi._check(lib.tdg_detect(ctx.handle, win._h, cs._h, 0.25, bench.FS, out, n_units))
         h = hash(bytes(out))
         same = "" if ref is None else (" same-detections" if h == ref else " DIFFERENT-detections")
         ref = h if ref is None else ref
