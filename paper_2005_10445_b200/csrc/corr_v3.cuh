@@ -53,6 +53,13 @@ constexpr int kGroup = 2;   // code pairs per pass-A item (sharing one window sp
 #ifndef TDG_B_SEP_TR
 #define TDG_B_SEP_TR 0
 #endif
+//   TDG_A_PIPE     pass A without the end-of-item CTA barrier: each warp
+//                  stores its own staged column (TMA) and releases the slot
+//                  through an "empty" mbarrier; thread 0 refills a slot once
+//                  all four warps released it
+#ifndef TDG_A_PIPE
+#define TDG_A_PIPE 0
+#endif
 constexpr int kSlots = TDG_NSLOT;
 
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
@@ -281,6 +288,23 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Desc& D, co
     if (act) fence_proxy_async_smem();
 }
 
+// lane 0 of a warp (TDG_A_PIPE): the TMA tensor store of this warp's own
+// staged column, if its role is active in the item
+template <int PA, int QA, int PB, int QB>
+__device__ __forceinline__ void store_passA_role(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl,
+                                                 int role) {
+    using F = Fused<PA, QA, PB, QB>;
+    constexpr int N1 = F::LB;
+    const int cp = k.idx / S.ngw;
+    const CorrGroup<kGroup>& gd = D.groups[k.idx % S.ngw];
+    const bool self = (cp == 0) || (2 * cp == N1);
+    const int g = role >> 1, col = role & 1;
+    if (g < gd.npairs && (col == 0 || !self)) {
+        tma_store_4d(&S.mstore, sl + (1 + role) * F::XS, 0, col ? N1 - cp : cp, 0, gd.Mi[g]);
+        bulk_commit();
+    }
+}
+
 // thread 0, after the end-of-item barrier: one TMA tensor store per active
 // (pair, column) role of the item staged in slot sl
 template <int PA, int QA, int PB, int QB>
@@ -449,6 +473,8 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
+        mbar_init(&bar[2], F::NT / 32);
+        mbar_init(&bar[3], F::NT / 32);
         mbar_fence_init();
         if (i0 < i1) {
             const Desc Dg{S.groups, S.outs};
@@ -472,6 +498,50 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
     if (TYPE == 1 && TDG_B_TW_SMEM)
         for (int i = threadIdx.x; i < F::LB; i += F::NT) twb[i] = __ldg(&S.twB[i]);
     __syncthreads();
+    if (TYPE == 0 && TDG_A_PIPE && kSlots == 2) {
+        // bar[0..1]: slot full (TMA bytes); bar[2..3]: slot released by all
+        // four warps.  Item j lives in slot j & 1; during item j (after step
+        // 1) every warp releases the slot of item j - 1 and thread 0 refills
+        // it with item j + 1.  No CTA-wide barrier inside the loop.
+        uint64_t* empty = bar + 2;
+        uint32_t full_ph = 0u, empty_ph = 0u;
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int item = i0, j = 0; item < i1; ++item, ++j) {
+            const int s = j & 1;
+            auto refill = [&]() {
+                if (item + 1 >= i1) return;
+                const int t = s ^ 1;   // slot of item j - 1, to hold item j + 1
+                if (j >= 1) {
+                    if (lane == 0) {
+                        bulk_wait_read_all();   // this warp's store of item j - 1 has read its staging
+                        mbar_arrive(&empty[t]);
+                    }
+                    if (threadIdx.x == 0) {
+                        mbar_wait(&empty[t], (empty_ph >> t) & 1u);
+                    }
+                    empty_ph ^= 1u << t;
+                }
+                if (threadIdx.x == 0) {
+                    const Ticket kn{TYPE, 0, item + 1};
+                    if (!ticket_noop(S, D, kn))
+                        issue_ticket<PA, QA, PB, QB>(S, D, kn, slots + size_t(t) * F::SLOT, &bar[t]);
+                }
+            };
+            const Ticket k{TYPE, 0, item};
+            if (ticket_noop(S, D, k)) {
+                refill();
+                continue;
+            }
+            float2* sl = slots + size_t(s) * F::SLOT;
+            mbar_wait(&bar[s], (full_ph >> s) & 1u);
+            full_ph ^= 1u << s;
+            item_passA<PA, QA, PB, QB>(S, D, k, sl, refill);
+            __syncwarp();
+            if (lane == 0) store_passA_role<PA, QA, PB, QB>(S, D, k, sl, warp);
+        }
+        if (lane == 0) bulk_wait_all();
+        return;
+    }
     uint32_t phases = 0u;   // bit s: parity of slot s's mbarrier
     for (int item = i0, s = 0; item < i1; ++item, s ^= (kSlots - 1)) {
         // next item's bulk copies into slot s^1 (two slots): pass B at the
