@@ -78,9 +78,23 @@ __host__ __device__ constexpr int up16(int x) { return (x + 15) & ~15; }   // fl
 // [w_N^{+k1 c}, c < QA][w_N^{+k1 QA e}, e < PA], padded to a 16-byte multiple.
 __host__ __device__ constexpr int inter_tw_stride(int PA, int QA) { return even_up(PA + QA); }
 
+__host__ __device__ constexpr int cgcd(int a, int b) { return b ? cgcd(b, a % b) : a; }
+
+// Prime-factor (Good-Thomas) split of the correlation length: when the pass-A
+// step-1 lane dimension PA is coprime to N / PA = N1 * QA (the search shape:
+// N = 27 x 32768), the inverse DFT is DFT_PA (x) DFT_{N/PA} with no twiddles
+// between them, and DFT_{N/PA} is the four-step N1 x QA.  Spectra are then
+// stored per column k1 = k mod N1 in PFA order (element a + PA*b for
+// a = k mod PA, b = (k mod N1*QA) div N1), pass A runs DFT_QA over b and
+// DFT_PA over a without step-2 twiddles and with an inter-pass twiddle
+// w_{N/PA}^{k1 c} that is constant per lane, and output t_a, t_b map to the
+// lag t = ((N/PA) t_a + PA t_b) mod N.
+__host__ __device__ constexpr bool pfa_split(int PA, int QA, int N1) { return PA > 1 && cgcd(PA, N1 * QA) == 1; }
+
 template <int PA, int QA, int PB, int QB>
 struct Fused {
     static constexpr int LA = PA * QA, LB = PB * QB;
+    static constexpr bool PFA = pfa_split(PA, QA, LB);
     static constexpr int QSA = qstride_even_pad(QA);
     static constexpr int TWS = inter_tw_stride(PA, QA);
     // pass-A slot: [D column][X columns: 2 per pair][2 twiddle rows], every
@@ -215,7 +229,32 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Desc& D, co
     // ---- step 1: lane a: product + Q-point IDFT over rows r = a + P*b
     float2 v[Q];
     const bool act1 = act && lane < P;
-    if (act1) {
+    if (act1 && F::PFA) {
+        // PFA order: element (a, b) at a + P*b; the mirror N - k of (a, b) is
+        // ((P - a) % P, Q - 1 - b) across a column pair, ((P - a) % P, (Q - b) % Q)
+        // in column 0
+        const int a = lane;
+        const int am = a ? P - a : 0;
+        const float2* D = sl;
+        const float2* Xm = sl + (1 + 2 * g) * F::XS;   // X column N1-cp (or cp if self)
+        if (col == 0) {
+            if (cp == 0) {
+#pragma unroll
+                for (int b = 0; b < Q; ++b) v[b] = cmul(D[a + P * b], Xm[am + P * ((Q - b) % Q)]);
+            } else {
+#pragma unroll
+                for (int b = 0; b < Q; ++b) v[b] = cmul(D[a + P * b], Xm[am + P * (Q - 1 - b)]);
+            }
+        } else {
+            const float2* Xc = sl + (2 + 2 * g) * F::XS;  // X column cp
+#pragma unroll
+            for (int b = 0; b < Q; ++b) {
+                const int m = am + P * (Q - 1 - b);   // source element of output (a, b)
+                v[b] = cmulc(Xc[m], D[m]);
+            }
+        }
+        dft<Q, +1>(v);
+    } else if (act1) {
         const int a = lane;
         const float2* D = sl;
         const float2* Xm = sl + (1 + 2 * g) * F::XS;   // X column N1-cp (or cp if self)
@@ -260,10 +299,20 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Desc& D, co
         float2 w[P];
 #pragma unroll
         for (int a = 0; a < P; ++a) w[a] = tr[a * QS];
-        apply_step2_twiddles<P, Q>(w, S.twA, c);
+        if (!F::PFA) apply_step2_twiddles<P, Q>(w, S.twA, c);
         dft<P, +1>(w);
         const float2* twr = sl + F::A_OPS + col * TWS;
         const float2 tc = twr[c];
+        if (F::PFA) {
+            // inter-pass twiddle w_{N/P}^{k1 c}: one value per lane (twr row k1
+            // holds w_N^{k1 P c}, c < Q)
+            float2* stg = sl + (1 + role) * F::XS;
+            __syncwarp(0xffffffffu >> (32 - Q));
+#pragma unroll
+            for (int e = 0; e < P; ++e) stg[c + Q * e] = cmul(w[e], tc);
+            fence_proxy_async_smem();
+            return;
+        }
         // stage the column in t2 order in the warp's own region, then one TMA
         // tensor store scatters it into M's tile-major layout (N2/4 chunks of
         // 32 bytes) without occupying the LSU pipe
@@ -363,6 +412,7 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
     const int t2 = tb * TB + t2l;
     float best_a = -1.f, best_b = -1.f;
     int e_lim = 0;
+    uint32_t pfa_base = 0, pfa_mask = 0;   // PFA: lag of e = 0 and valid-e mask
     float2 w[P];
     if (c < Q) {
 #pragma unroll
@@ -374,6 +424,39 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
             apply_step2_twiddles<P, Q>(w, S.twB, c);
         }
         dft<P, +1>(w);
+        if (F::PFA) {
+            // column t2 = t_b1 + QA t_a; outputs e are lags
+            // t = ((N/PA) t_a + PA (t_b1 + QA (c + Q e))) mod N = (base + e*SE) mod N
+            constexpr uint32_t NN = uint32_t(F::LA) * uint32_t(F::LB), SE = NN / P;
+            constexpr uint32_t NBB = NN / PA;
+            const uint32_t tb1 = uint32_t(t2) % uint32_t(QA), ta = uint32_t(t2) / uint32_t(QA);
+            pfa_base = uint32_t((uint64_t(NBB) * ta + uint64_t(PA) * (tb1 + uint32_t(QA) * uint32_t(c))) % NN);
+            // valid lags t < W: e < e1 (before the wrap at e_w) and e in [e_w, e2)
+            const uint32_t e_w = (NN - pfa_base + SE - 1) / SE;
+            const uint32_t e_1 = W > pfa_base ? min(e_w, (W - pfa_base + SE - 1) / SE) : 0u;
+            const uint32_t e_2 = min(uint32_t(P), uint32_t((uint64_t(W) + NN - pfa_base + SE - 1) / SE));
+            auto low = [](uint32_t k) { return k >= 32u ? 0xffffffffu : (1u << k) - 1u; };
+            pfa_mask = low(e_1) | (e_2 > e_w ? low(e_2) & ~low(e_w) : 0u);
+            if (S.write_xc) {
+#pragma unroll
+                for (int e = 0; e < P; ++e) {
+                    if ((pfa_mask >> e) & 1u) {
+                        uint32_t t = pfa_base + uint32_t(e) * SE;
+                        t = t >= NN ? t - NN : t;
+                        if (po.xc_a) po.xc_a[t] = w[e].x * S.inv_n;
+                        if (po.xc_b) po.xc_b[t] = w[e].y * S.inv_n;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < P; ++e) {
+                    if ((pfa_mask >> e) & 1u) {
+                        best_a = fmaxf(best_a, fabsf(w[e].x));
+                        best_b = fmaxf(best_b, fabsf(w[e].y));
+                    }
+                }
+            }
+        } else
         // valid lags t = t2 + N2*(c + Q*e) < W form a prefix e < e_lim
         if (t2 < N2 && uint32_t(t2) < W) {
             const int t1max = int((W - 1u - uint32_t(t2)) / uint32_t(N2));
@@ -421,7 +504,35 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
         // shuffles) is taken by every lane or none
         const bool need_a = __any_sync(0xffffffffu, best_a >= 0.f && best_a >= cur_a);
         const bool need_b = __any_sync(0xffffffffu, best_b >= 0.f && po.key_b != nullptr && best_b >= cur_b);
-        if (need_a || need_b) {   // warp-uniform
+        if (F::PFA && (need_a || need_b)) {   // warp-uniform
+            // smallest lag among this lane's maxima (lags are not monotone in e)
+            constexpr uint32_t NN = uint32_t(F::LA) * uint32_t(F::LB), SE = NN / P;
+            uint32_t ta = 0xffffffffu, tb = 0xffffffffu;
+            if (c < Q) {
+#pragma unroll
+                for (int e = 0; e < P; ++e) {
+                    if ((pfa_mask >> e) & 1u) {
+                        uint32_t t = pfa_base + uint32_t(e) * SE;
+                        t = t >= NN ? t - NN : t;
+                        if (fabsf(w[e].x) == best_a) ta = min(ta, t);
+                        if (fabsf(w[e].y) == best_b) tb = min(tb, t);
+                    }
+                }
+            }
+            unsigned long long ka = need_a && ta != 0xffffffffu ? peak_key(best_a, ta) : 0ull;
+            unsigned long long kb = need_b && tb != 0xffffffffu ? peak_key(best_b, tb) : 0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const unsigned long long xa = __shfl_xor_sync(0xffffffffu, ka, o);
+                const unsigned long long xb = __shfl_xor_sync(0xffffffffu, kb, o);
+                ka = xa > ka ? xa : ka;
+                kb = xb > kb ? xb : kb;
+            }
+            if ((tid & 31) == 0) {
+                if (ka) atomicMax(po.key_a, ka);
+                if (kb) atomicMax(po.key_b, kb);
+            }
+        } else if (need_a || need_b) {   // warp-uniform
             int ea = P, eb = P;
             if (c < Q) {
 #pragma unroll

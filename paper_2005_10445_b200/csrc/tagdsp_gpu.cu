@@ -323,7 +323,7 @@ void launch_fwd1(int L, unsigned n_seq, cudaStream_t st, const tdg::SeqPairDesc*
 }
 
 void launch_fwd2(int L, bool split, dim3 grid, cudaStream_t st, const tdg::SeqPairDesc* pairs, int N1,
-                 const float2* tw, const float2* twI) {
+                 const float2* tw, const float2* twI, bool pfa) {
     switch (L) {
 #define X(LL, P, Q)                                                                                       \
     case LL: {                                                                                            \
@@ -331,10 +331,10 @@ void launch_fwd2(int L, bool split, dim3 grid, cudaStream_t st, const tdg::SeqPa
         const size_t sm = (size_t(2) * P * QS + 2 * LL + 2 * (P + Q)) * sizeof(float2);                   \
         if (split) {                                                                                      \
             set_smem(tdg::k_fwd_pass2<P, Q, true>, sm);                                                   \
-            if (STREAM_OPS) tdg::k_fwd_pass2<P, Q, true><<<grid, block_for(2 * std::max(P, Q)), sm, st>>>(pairs, N1, tw, twI); \
+            if (STREAM_OPS) tdg::k_fwd_pass2<P, Q, true><<<grid, block_for(2 * std::max(P, Q)), sm, st>>>(pairs, N1, tw, twI, pfa); \
         } else {                                                                                          \
             set_smem(tdg::k_fwd_pass2<P, Q, false>, sm);                                                  \
-            if (STREAM_OPS) tdg::k_fwd_pass2<P, Q, false><<<grid, block_for(2 * std::max(P, Q)), sm, st>>>(pairs, N1, tw, twI); \
+            if (STREAM_OPS) tdg::k_fwd_pass2<P, Q, false><<<grid, block_for(2 * std::max(P, Q)), sm, st>>>(pairs, N1, tw, twI, pfa); \
         }                                                                                                 \
         LAUNCHED();                                                                                       \
         return;                                                                                           \
@@ -662,9 +662,12 @@ struct tdg_ctx {
         const long long N = (long long)N1 * N2;
         std::vector<float2> h(size_t(N1) * tws, make_float2(0.f, 0.f));
         const double pi = 3.14159265358979323846;
+        // prime-factor split (corr_v3.cuh pfa_split): row k1 = [w_N^{+k1 P c}, c < QA]
+        const bool pfa = tdg::pfa_split(s.P, s.Q, N1);
         for (int k1 = 0; k1 < N1; ++k1)
             for (int r = 0; r < s.P + s.Q; ++r) {
-                const long long e = (r < s.Q ? (long long)k1 * r : (long long)k1 * s.Q * (r - s.Q)) % N;
+                const long long e = (pfa ? (r < s.Q ? (long long)k1 * s.P * r : 0)
+                                         : r < s.Q ? (long long)k1 * r : (long long)k1 * s.Q * (r - s.Q)) % N;
                 const double ang = 2.0 * pi * double(e) / double(N);
                 h[size_t(k1) * tws + r] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
             }
@@ -908,7 +911,8 @@ void run_forward(tdg_ctx* ctx, int N1, int N2, const std::vector<FwdJob>& jobs, 
         }
         {
             KScope ks(ctx, "fwd_pass2");
-            launch_fwd2(N2, split, dim3(unsigned(N1 / 2 + 1), unsigned(n)), ctx->stream, dd + base, N1, tw2, twI);
+            launch_fwd2(N2, split, dim3(unsigned(N1 / 2 + 1), unsigned(n)), ctx->stream, dd + base, N1, tw2, twI,
+                        tdg::pfa_split(shape_of(N2).P, shape_of(N2).Q, N1));
         }
         if (chunk_done) {
             const size_t k = chunk_done->size();
