@@ -60,6 +60,15 @@ constexpr int kGroup = 2;   // code pairs per pass-A item (sharing one window sp
 #ifndef TDG_A_PIPE
 #define TDG_A_PIPE 0
 #endif
+//   TDG_A_SPLIT    pass A: every warp issues its own share of an item's bulk
+//                  copies (its X column; warp 0 the window column, warp 1
+//                  the twiddle rows) and the TMA store of its own staged
+//                  column, instead of thread 0 issuing all of them (which
+//                  made warp 0 ~25 % longer than the others and left them
+//                  waiting at the end-of-item barrier)
+#ifndef TDG_A_SPLIT
+#define TDG_A_SPLIT 1
+#endif
 constexpr int kSlots = TDG_NSLOT;
 
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
@@ -112,7 +121,8 @@ struct Fused {
     static constexpr int B_TW = TDG_B_TW_SMEM ? up16(LB) : 0;               // pass-B twiddle table
     static constexpr int NT = 128;
     // slots, then (pass B) the transpose region and the twiddle table
-    static constexpr size_t SMEM = 128 + kSlots * size_t(SLOT) * 8 + size_t(B_TR + B_TW) * 8;
+    static constexpr int ANC = 4 * cmax(QA, QB);                             // step-2 twiddle anchors
+    static constexpr size_t SMEM = 128 + kSlots * size_t(SLOT) * 8 + size_t(B_TR + B_TW + ANC) * 8;
     static_assert(cmax(PA, QA) <= 32 && cmax(PB, QB) <= 32, "one warp per column role");
     static_assert(LA % kTileB == 0, "M tiles cover the t2 columns exactly (TMA store box)");
     static_assert(kTileB * cmax(PB, QB) <= NT, "pass-B tasks fit the CTA");
@@ -203,6 +213,36 @@ __device__ __forceinline__ void issue_ticket(const CorrSched& S, const Desc& D, 
     }
 }
 
+// lane 0 of warp `role` (TDG_A_SPLIT): this role's share of a pass-A item's
+// bulk copies, with one arrive.expect_tx on the slot's barrier (initialised
+// for NT/32 arrivals)
+template <int PA, int QA, int PB, int QB>
+__device__ __forceinline__ void issue_passA_role(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl,
+                                                 uint64_t* bar, int role) {
+    using F = Fused<PA, QA, PB, QB>;
+    constexpr int LA = F::LA, TWS = F::TWS;
+    fence_proxy_async_smem();
+    const int cp = k.idx / S.ngw;
+    const CorrGroup<kGroup>& gd = D.groups[k.idx % S.ngw];
+    const bool self = (cp == 0) || (2 * cp == F::LB);
+    const int g = role >> 1, col = role & 1;
+    const bool act = g < gd.npairs && (col == 0 || !self);
+    uint32_t bytes = act ? uint32_t(LA) * 8u : 0u;
+    if (role == 0) bytes += uint32_t(LA) * 8u;
+    if (role == 1) bytes += 2u * TWS * 8u;
+    mbar_arrive_expect_tx(bar, bytes);
+    if (role == 0) bulk_g2s_hint(sl, gd.D + size_t(cp) * LA, LA * 8, bar, policy_evict_first());
+    if (act) {
+        const int xcol = (col == 0 && !self) ? F::LB - cp : cp;   // region 1 + role: X column of (g, col)
+        bulk_g2s_hint(sl + (1 + role) * F::XS, gd.Ca[g] + size_t(xcol) * LA, LA * 8, bar, policy_evict_last());
+    }
+    if (role == 1) {
+        const int k1b = cp == 0 ? 0 : F::LB - cp;
+        bulk_g2s(sl + F::A_OPS, S.twI + size_t(cp) * TWS, TWS * 8, bar);
+        bulk_g2s(sl + F::A_OPS + TWS, S.twI + size_t(k1b) * TWS, TWS * 8, bar);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Pass A item: column pair (cp, N1-cp) x up to kGroup code pairs of one
 // window.  Code pairs are stored as the full spectrum X = FFT(dc_a + i dc_b)
@@ -213,7 +253,8 @@ __device__ __forceinline__ void issue_ticket(const CorrSched& S, const Desc& D, 
 // tile-major M[(t2/kTileB)*N1*kTileB + k1*kTileB + t2%kTileB], times the
 // inter-pass twiddle w_N^{+k1 t2}.
 template <int PA, int QA, int PB, int QB, class Mid>
-__device__ __forceinline__ void item_passA(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl, Mid&& mid) {
+__device__ __forceinline__ void item_passA(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl, Mid&& mid,
+                                           const float2* anc) {
     using F = Fused<PA, QA, PB, QB>;
     constexpr int P = PA, Q = QA, L = F::LA, QS = F::QSA, TWS = F::TWS;
     constexpr int N1 = F::LB;   // pass-B length == number of columns
@@ -229,11 +270,16 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Desc& D, co
     // ---- step 1: lane a: product + Q-point IDFT over rows r = a + P*b
     float2 v[Q];
     const bool act1 = act && lane < P;
+    // row of this lane.  PFA: half-warp 0 takes rows 1..16, half-warp 1 rows
+    // 0, 17..P-1, so that both a row's elements a + P*b and its mirror's
+    // (P - a) % P + P*b' hit 16 distinct bank pairs per half-warp (lane a = row
+    // a put rows 0 and 16 of the mirror into one bank pair: 1.5x wavefronts)
+    const int arow = (F::PFA && P > 16) ? (lane < 16 ? lane + 1 : (lane == 16 ? 0 : lane)) : lane;
     if (act1 && F::PFA) {
         // PFA order: element (a, b) at a + P*b; the mirror N - k of (a, b) is
         // ((P - a) % P, Q - 1 - b) across a column pair, ((P - a) % P, (Q - b) % Q)
         // in column 0
-        const int a = lane;
+        const int a = arow;
         const int am = a ? P - a : 0;
         const float2* D = sl;
         const float2* Xm = sl + (1 + 2 * g) * F::XS;   // X column N1-cp (or cp if self)
@@ -285,7 +331,7 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Desc& D, co
     // the transpose goes over this warp's own X column (read only by it)
     __syncwarp();
     if (act1) {
-        float2* tr = sl + (1 + role) * F::XS + lane * QS;
+        float2* tr = sl + (1 + role) * F::XS + arow * QS;
 #pragma unroll
         for (int c = 0; c < Q; ++c) tr[c] = v[c];
     }
@@ -299,7 +345,7 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Desc& D, co
         float2 w[P];
 #pragma unroll
         for (int a = 0; a < P; ++a) w[a] = tr[a * QS];
-        if (!F::PFA) apply_step2_twiddles<P, Q>(w, S.twA, c);
+        if (!F::PFA) apply_step2_twiddles_anc<P, Q>(w, anc, c);
         dft<P, +1>(w);
         const float2* twr = sl + F::A_OPS + col * TWS;
         const float2 tc = twr[c];
@@ -377,7 +423,7 @@ __device__ __forceinline__ void store_passA(const CorrSched& S, const Desc& D, c
 // the full xc rows (batch_xcorr diagnostics).
 template <int PA, int QA, int PB, int QB>
 __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl,
-                                           float2* trb, const float2* twb) {
+                                           float2* trb, const float2* twb, const float2* anc) {
     using F = Fused<PA, QA, PB, QB>;
     constexpr int P = PB, Q = QB, ROW = F::ROWB, TB = kTileB;
     const CorrPairOut& po = D.outs[k.idx / S.n_tiles];
@@ -421,7 +467,7 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
 #pragma unroll
             for (int a = 1; a < P; ++a) w[a] = cmul(w[a], twb[a * Q + c]);
         } else {
-            apply_step2_twiddles<P, Q>(w, S.twB, c);
+            apply_step2_twiddles_anc<P, Q>(w, anc, c);
         }
         dft<P, +1>(w);
         if (F::PFA) {
@@ -574,6 +620,7 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
     float2* slots = reinterpret_cast<float2*>(smraw + 128);
     float2* trb = slots + size_t(kSlots) * F::SLOT;   // pass B: separate transpose region (TDG_B_SEP_TR)
     float2* twb = trb + F::B_TR;                      // pass B: twiddle table (TDG_B_TW_SMEM)
+    float2* anc = twb + F::B_TW;                      // step-2 twiddle anchors of this pass
     // the wave's descriptors live in shared memory (read by every item)
     unsigned char* dsm = smraw + F::SMEM;
     const int n_items = TYPE == 0 ? S.nA : S.nB;
@@ -581,16 +628,25 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
     const int i1 = int(int64_t(blockIdx.x + 1) * n_items / gridDim.x);
     // thread 0 starts the first item's bulk copies from the global descriptors
     // while the CTA stages the descriptors in shared memory
+    constexpr bool SPLIT = TYPE == 0 && TDG_A_SPLIT && !TDG_A_PIPE && kSlots == 2;
     if (threadIdx.x == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        mbar_init(&bar[0], SPLIT ? F::NT / 32 : 1);
+        mbar_init(&bar[1], SPLIT ? F::NT / 32 : 1);
         mbar_init(&bar[2], F::NT / 32);
         mbar_init(&bar[3], F::NT / 32);
         mbar_fence_init();
-        if (i0 < i1) {
+        if (!SPLIT && i0 < i1) {
             const Desc Dg{S.groups, S.outs};
             const Ticket k0{TYPE, 0, i0};
             if (!ticket_noop(S, Dg, k0)) issue_ticket<PA, QA, PB, QB>(S, Dg, k0, slots, &bar[0]);
+        }
+    }
+    if (SPLIT) {
+        __syncthreads();   // barriers initialised before any warp arrives on them
+        if ((threadIdx.x & 31) == 0 && i0 < i1) {
+            const Desc Dg{S.groups, S.outs};
+            const Ticket k0{TYPE, 0, i0};
+            if (!ticket_noop(S, Dg, k0)) issue_passA_role<PA, QA, PB, QB>(S, Dg, k0, slots, &bar[0], threadIdx.x >> 5);
         }
     }
     Desc D;
@@ -608,6 +664,10 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
     }
     if (TYPE == 1 && TDG_B_TW_SMEM)
         for (int i = threadIdx.x; i < F::LB; i += F::NT) twb[i] = __ldg(&S.twB[i]);
+    if (TYPE == 1)
+        fill_twiddle_anchors<PB, QB>(anc, S.twB, threadIdx.x, F::NT);
+    else if (!F::PFA)
+        fill_twiddle_anchors<PA, QA>(anc, S.twA, threadIdx.x, F::NT);
     __syncthreads();
     if (TYPE == 0 && TDG_A_PIPE && kSlots == 2) {
         // bar[0..1]: slot full (TMA bytes); bar[2..3]: slot released by all
@@ -646,7 +706,7 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
             float2* sl = slots + size_t(s) * F::SLOT;
             mbar_wait(&bar[s], (full_ph >> s) & 1u);
             full_ph ^= 1u << s;
-            item_passA<PA, QA, PB, QB>(S, D, k, sl, refill);
+            item_passA<PA, QA, PB, QB>(S, D, k, sl, refill, anc);
             __syncwarp();
             if (lane == 0) store_passA_role<PA, QA, PB, QB>(S, D, k, sl, warp);
         }
@@ -660,6 +720,16 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
         // TMA stores of the item that last used slot s^1 have read their
         // staging area.  One slot: after this item (below).
         auto prefetch = [&]() {
+            if (SPLIT) {
+                if ((threadIdx.x & 31) == 0 && item + 1 < i1) {
+                    bulk_wait_read_all();   // this warp's store of the slot's last item has read it
+                    const Ticket kn{TYPE, 0, item + 1};
+                    if (!ticket_noop(S, D, kn))
+                        issue_passA_role<PA, QA, PB, QB>(S, D, kn, slots + size_t(s ^ 1) * F::SLOT, &bar[s ^ 1],
+                                                         threadIdx.x >> 5);
+                }
+                return;
+            }
             if (kSlots == 2 && threadIdx.x == 0 && item + 1 < i1) {
                 if (TYPE == 0) bulk_wait_read_all();
                 const Ticket kn{TYPE, 0, item + 1};
@@ -685,7 +755,7 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
         mbar_wait(&bar[s], (phases >> s) & 1u);
         phases ^= 1u << s;
         if (TYPE == 0) {
-            item_passA<PA, QA, PB, QB>(S, D, k, sl, prefetch);
+            item_passA<PA, QA, PB, QB>(S, D, k, sl, prefetch, anc);
         } else {
             // the M tile is in shared memory and its L2 lines are dead: drop
             // them without a DRAM write-back.  Only lines wholly inside the
@@ -699,13 +769,17 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
             if (S.discard)
                 for (uintptr_t a = lo + uintptr_t(threadIdx.x) * 128; a < hi; a += uintptr_t(F::NT) * 128)
                     discard_l2(reinterpret_cast<const void*>(a));
-            item_passB<PA, QA, PB, QB>(S, D, k, sl, trb, twb);
+            item_passB<PA, QA, PB, QB>(S, D, k, sl, trb, twb, anc);
         }
         __syncthreads();   // slot s consumed (pass A: its staged columns complete)
-        if (TYPE == 0 && threadIdx.x == 0) store_passA<PA, QA, PB, QB>(S, D, k, sl);
+        if (SPLIT) {
+            if ((threadIdx.x & 31) == 0) store_passA_role<PA, QA, PB, QB>(S, D, k, sl, threadIdx.x >> 5);
+        } else if (TYPE == 0 && threadIdx.x == 0) {
+            store_passA<PA, QA, PB, QB>(S, D, k, sl);
+        }
         prefetch_after();
     }
-    if (TYPE == 0 && threadIdx.x == 0) bulk_wait_all();
+    if (TYPE == 0 && (SPLIT ? (threadIdx.x & 31) == 0 : threadIdx.x == 0)) bulk_wait_all();
 }
 
 }  // namespace tdg

@@ -1,0 +1,4 @@
+OUT=gpurun_out/${TAG:-r02f}; mkdir -p $OUT
+TDG_LIB_PATH=abtest/lib_${PV:-S}.so TDG_PARITY_OUT=$OUT timeout 900 python -m pytest tests -x -q -m gpu -rs --deselect tests/test_gpu_dist_two_rank.py::test_two_ranks_one_gpu_match_single_rank > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+bash tools/ab_libs.sh $OUT detect ${VARS:-N S}
+nvidia-smi > $OUT/smi_end.txt 2>&1
