@@ -15,13 +15,15 @@
 // spectra stream through (evict_first), and pass B drops each M tile from L2
 // after reading it (discard: no DRAM write-back of dead data).
 //
-// Inside a CTA, thread 0 prefetches the next item's operands with 1-D bulk
-// copies (cp.async.bulk -> UBLKCP, completing on an mbarrier) into the
-// second shared-memory slot while the 4 warps run the current item from the
-// first.  Pass-A inter-pass twiddles come from a precomputed table that rides
-// in the same bulk copies, so no item recomputes sincos.  In pass A each warp
-// (one column role) transposes and stages over the X column only it reads, so
-// an item has a single CTA barrier (at its end).
+// Inside a CTA, the next item's operands are bulk-copied (cp.async.bulk ->
+// UBLKCP, completing on an mbarrier) into the second shared-memory slot while
+// the 4 warps run the current item from the first: in pass A every warp's
+// lane 0 issues its own share (its X column; warp 0 the window column, warp 1
+// the twiddle rows) and the TMA store of its own staged column, in pass B
+// thread 0 issues the tile.  In pass A each warp (one column role) transposes
+// and stages over the X column only it reads, so an item has a single CTA
+// barrier (at its end).  The search shape (N = 27 x 32768) runs as a
+// prime-factor split: no step-2 twiddles in pass A (pfa_split below).
 #pragma once
 #include "kernels.cuh"
 #include "tma.cuh"
@@ -31,45 +33,18 @@ namespace tdg {
 constexpr int kTileB = 4;   // t2 columns per pass-B tile (M is stored tile-major)
 constexpr int kGroup = 2;   // code pairs per pass-A item (sharing one window spectrum column)
 
-// Build-time layout variants (A/B-timed with tools/ab_libs.sh; the defaults
-// are the measured best):
-//   TDG_NSLOT      operand slots per CTA: 2 = the next item's bulk copies
-//                  overlap this item; 1 = half the shared memory, so more
-//                  CTAs per SM overlap each other instead
-//   TDG_CORR_MINB  CTAs per SM the register budget is sized for
-//   TDG_B_TW_SMEM  pass-B step-2 twiddles from a shared-memory table filled
-//                  once per CTA (instead of chained products)
-//   TDG_B_SEP_TR   pass-B transposes into their own region (one CTA barrier
-//                  per item fewer)
-#ifndef TDG_NSLOT
-#define TDG_NSLOT 2
-#endif
+// Build-time layout variant (A/B-timed with tools/ab_libs.sh):
+//   TDG_CORR_MINB  CTAs per SM the register budget is sized for (3: 170
+//                  registers; 4 spills and measured 13-17 % slower)
+// Two operand slots per CTA: the next item's bulk copies overlap this item.
+// Measured and removed: one slot with more CTAs per SM, pass-B
+// twiddles from a full shared-memory table (-20 %: every twiddle an LDS),
+// pass-B transposes in a separate region, pass A without the end-of-item
+// barrier (per-warp slot release through "empty" mbarriers).
 #ifndef TDG_CORR_MINB
 #define TDG_CORR_MINB 3
 #endif
-#ifndef TDG_B_TW_SMEM
-#define TDG_B_TW_SMEM 0
-#endif
-#ifndef TDG_B_SEP_TR
-#define TDG_B_SEP_TR 0
-#endif
-//   TDG_A_PIPE     pass A without the end-of-item CTA barrier: each warp
-//                  stores its own staged column (TMA) and releases the slot
-//                  through an "empty" mbarrier; thread 0 refills a slot once
-//                  all four warps released it
-#ifndef TDG_A_PIPE
-#define TDG_A_PIPE 0
-#endif
-//   TDG_A_SPLIT    pass A: every warp issues its own share of an item's bulk
-//                  copies (its X column; warp 0 the window column, warp 1
-//                  the twiddle rows) and the TMA store of its own staged
-//                  column, instead of thread 0 issuing all of them (which
-//                  made warp 0 ~25 % longer than the others and left them
-//                  waiting at the end-of-item barrier)
-#ifndef TDG_A_SPLIT
-#define TDG_A_SPLIT 1
-#endif
-constexpr int kSlots = TDG_NSLOT;
+constexpr int kSlots = 2;
 
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int qstride_even_pad(int q) { return (q % 2) ? q : q + 1; }
@@ -115,14 +90,12 @@ struct Fused {
     static constexpr int A_OPS = (1 + 2 * kGroup) * XS;
     static constexpr int A_SLOT = up16(A_OPS + 2 * TWS);
     static constexpr int ROWB = passb_row(QB);
-    static constexpr int B_TR = TDG_B_SEP_TR ? up16(PB * ROWB) : 0;        // separate transpose region
-    static constexpr int B_SLOT = TDG_B_SEP_TR ? up16(LB * kTileB) : up16(cmax(LB * kTileB, PB * ROWB));
+    static constexpr int B_SLOT = up16(cmax(LB * kTileB, PB * ROWB));     // tile, transposed in place
     static constexpr int SLOT = cmax(A_SLOT, B_SLOT);
-    static constexpr int B_TW = TDG_B_TW_SMEM ? up16(LB) : 0;               // pass-B twiddle table
     static constexpr int NT = 128;
     // slots, then (pass B) the transpose region and the twiddle table
     static constexpr int ANC = 4 * cmax(QA, QB);                             // step-2 twiddle anchors
-    static constexpr size_t SMEM = 128 + kSlots * size_t(SLOT) * 8 + size_t(B_TR + B_TW + ANC) * 8;
+    static constexpr size_t SMEM = 128 + kSlots * size_t(SLOT) * 8 + size_t(ANC) * 8;
     static_assert(cmax(PA, QA) <= 32 && cmax(PB, QB) <= 32, "one warp per column role");
     static_assert(LA % kTileB == 0, "M tiles cover the t2 columns exactly (TMA store box)");
     static_assert(kTileB * cmax(PB, QB) <= NT, "pass-B tasks fit the CTA");
@@ -159,11 +132,19 @@ __device__ __forceinline__ int tid_x() {
     return t;
 }
 
+// An item's coordinates: pass A (u, v) = (column pair cp, group), item
+// u * ngw + v; pass B (u, v) = (pair, M tile), item u * n_tiles + v.  A CTA
+// walks a contiguous item range, so they advance without divisions.
 struct Ticket {
-    int type;   // 0 = pass A, 1 = pass B
-    int w;
-    int idx;
+    int u, v;
 };
+__device__ __forceinline__ Ticket ticket_at(int item, int den) { return Ticket{item / den, item % den}; }
+__device__ __forceinline__ void ticket_next(Ticket& t, int den) {
+    if (++t.v == den) {
+        t.v = 0;
+        ++t.u;
+    }
+}
 
 // the wave's descriptors, copied to shared memory once per CTA
 struct Desc {
@@ -171,49 +152,27 @@ struct Desc {
     const CorrPairOut* outs;
 };
 
-__device__ __forceinline__ bool ticket_noop(const CorrSched& S, const Desc& D, const Ticket& k) {
-    if (k.type == 0) return D.groups[k.idx % S.ngw].npairs == 0;
-    return D.outs[k.idx / S.n_tiles].M == nullptr;
+template <int TYPE>
+__device__ __forceinline__ bool ticket_noop(const Desc& D, const Ticket& k) {
+    if (TYPE == 0) return D.groups[k.v].npairs == 0;
+    return D.outs[k.u].M == nullptr;
 }
 
-// thread 0: bulk copies of a (non-noop, ready) item into slot sl
+// thread 0 (pass B): the bulk copy of a (non-noop) item's M tile into slot sl
 template <int PA, int QA, int PB, int QB>
-__device__ __forceinline__ void issue_ticket(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl,
-                                             uint64_t* bar) {
+__device__ __forceinline__ void issue_tile(const Desc& D, const Ticket& k, float2* sl, uint64_t* bar) {
     using F = Fused<PA, QA, PB, QB>;
+    constexpr int LB = F::LB;
     // earlier generic use of this slot before the async writes (no global
     // proxy fence: M is written by pass A's TMA stores and read by pass B's
     // bulk copies, both async proxy, across a kernel boundary)
     fence_proxy_async_smem();
-    if (k.type == 0) {
-        constexpr int LA = F::LA, TWS = F::TWS;
-        const int cp = k.idx / S.ngw;
-        const CorrGroup<kGroup>& gd = D.groups[k.idx % S.ngw];
-        const bool self = (cp == 0) || (2 * cp == F::LB);
-        const uint32_t bytes = uint32_t(LA) * 8u * uint32_t(1 + gd.npairs * (self ? 1 : 2)) + 2u * TWS * 8u;
-        mbar_arrive_expect_tx(bar, bytes);
-        // window spectrum: read by this wave only; code spectra: reused by
-        // the next waves (jobs are ordered code-pair-major)
-        const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
-        bulk_g2s_hint(sl, gd.D + size_t(cp) * LA, LA * 8, bar, pol_first);
-        for (int g = 0; g < gd.npairs; ++g) {
-            const float2* X = gd.Ca[g];
-            bulk_g2s_hint(sl + (1 + 2 * g) * F::XS, X + size_t(self ? cp : F::LB - cp) * LA, LA * 8, bar, pol_last);
-            if (!self) bulk_g2s_hint(sl + (2 + 2 * g) * F::XS, X + size_t(cp) * LA, LA * 8, bar, pol_last);
-        }
-        const int k1b = cp == 0 ? 0 : F::LB - cp;
-        bulk_g2s(sl + F::A_OPS, S.twI + size_t(cp) * TWS, TWS * 8, bar);
-        bulk_g2s(sl + F::A_OPS + TWS, S.twI + size_t(k1b) * TWS, TWS * 8, bar);
-    } else {
-        constexpr int LB = F::LB;
-        const CorrPairOut& po = D.outs[k.idx / S.n_tiles];
-        const int tb = k.idx % S.n_tiles;
-        mbar_arrive_expect_tx(bar, LB * kTileB * 8);
-        bulk_g2s_hint(sl, po.M + size_t(tb) * LB * kTileB, LB * kTileB * 8, bar, policy_evict_first());
-    }
+    const CorrPairOut& po = D.outs[k.u];
+    mbar_arrive_expect_tx(bar, LB * kTileB * 8);
+    bulk_g2s_hint(sl, po.M + size_t(k.v) * LB * kTileB, LB * kTileB * 8, bar, policy_evict_first());
 }
 
-// lane 0 of warp `role` (TDG_A_SPLIT): this role's share of a pass-A item's
+// lane 0 of warp `role`: this role's share of a pass-A item's
 // bulk copies, with one arrive.expect_tx on the slot's barrier (initialised
 // for NT/32 arrivals)
 template <int PA, int QA, int PB, int QB>
@@ -222,8 +181,8 @@ __device__ __forceinline__ void issue_passA_role(const CorrSched& S, const Desc&
     using F = Fused<PA, QA, PB, QB>;
     constexpr int LA = F::LA, TWS = F::TWS;
     fence_proxy_async_smem();
-    const int cp = k.idx / S.ngw;
-    const CorrGroup<kGroup>& gd = D.groups[k.idx % S.ngw];
+    const int cp = k.u;
+    const CorrGroup<kGroup>& gd = D.groups[k.v];
     const bool self = (cp == 0) || (2 * cp == F::LB);
     const int g = role >> 1, col = role & 1;
     const bool act = g < gd.npairs && (col == 0 || !self);
@@ -258,9 +217,9 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Desc& D, co
     using F = Fused<PA, QA, PB, QB>;
     constexpr int P = PA, Q = QA, L = F::LA, QS = F::QSA, TWS = F::TWS;
     constexpr int N1 = F::LB;   // pass-B length == number of columns
-    const int cp = k.idx / S.ngw;
+    const int cp = k.u;
     const int tid = tid_x();
-    const CorrGroup<kGroup>& gd = D.groups[k.idx % S.ngw];
+    const CorrGroup<kGroup>& gd = D.groups[k.v];
     const int npairs = gd.npairs;
     const bool self = (cp == 0) || (2 * cp == N1);
     const int role = tid >> 5;   // warp-uniform (g, col)
@@ -383,36 +342,21 @@ __device__ __forceinline__ void item_passA(const CorrSched& S, const Desc& D, co
     if (act) fence_proxy_async_smem();
 }
 
-// lane 0 of a warp (TDG_A_PIPE): the TMA tensor store of this warp's own
+// lane 0 of a warp, after the end-of-item barrier: the TMA tensor store of this warp's own
 // staged column, if its role is active in the item
 template <int PA, int QA, int PB, int QB>
 __device__ __forceinline__ void store_passA_role(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl,
                                                  int role) {
     using F = Fused<PA, QA, PB, QB>;
     constexpr int N1 = F::LB;
-    const int cp = k.idx / S.ngw;
-    const CorrGroup<kGroup>& gd = D.groups[k.idx % S.ngw];
+    const int cp = k.u;
+    const CorrGroup<kGroup>& gd = D.groups[k.v];
     const bool self = (cp == 0) || (2 * cp == N1);
     const int g = role >> 1, col = role & 1;
     if (g < gd.npairs && (col == 0 || !self)) {
         tma_store_4d(&S.mstore, sl + (1 + role) * F::XS, 0, col ? N1 - cp : cp, 0, gd.Mi[g]);
         bulk_commit();
     }
-}
-
-// thread 0, after the end-of-item barrier: one TMA tensor store per active
-// (pair, column) role of the item staged in slot sl
-template <int PA, int QA, int PB, int QB>
-__device__ __forceinline__ void store_passA(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl) {
-    using F = Fused<PA, QA, PB, QB>;
-    constexpr int N1 = F::LB;
-    const int cp = k.idx / S.ngw;
-    const CorrGroup<kGroup>& gd = D.groups[k.idx % S.ngw];
-    const bool self = (cp == 0) || (2 * cp == N1);
-    for (int g = 0; g < gd.npairs; ++g)
-        for (int col = 0; col < (self ? 1 : 2); ++col)
-            tma_store_4d(&S.mstore, sl + (1 + 2 * g + col) * F::XS, 0, col ? N1 - cp : cp, 0, gd.Mi[g]);
-    bulk_commit();
 }
 
 // ---------------------------------------------------------------------------
@@ -423,11 +367,11 @@ __device__ __forceinline__ void store_passA(const CorrSched& S, const Desc& D, c
 // the full xc rows (batch_xcorr diagnostics).
 template <int PA, int QA, int PB, int QB>
 __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl,
-                                           float2* trb, const float2* twb, const float2* anc) {
+                                           const float2* anc) {
     using F = Fused<PA, QA, PB, QB>;
     constexpr int P = PB, Q = QB, ROW = F::ROWB, TB = kTileB;
-    const CorrPairOut& po = D.outs[k.idx / S.n_tiles];
-    const int tb = k.idx % S.n_tiles;
+    const CorrPairOut& po = D.outs[k.u];
+    const int tb = k.v;
     const int tid = tid_x();
     constexpr int N2 = F::LA;   // pass-A length == number of t2 columns
     // the pair's best magnitudes so far (high words of the packed keys)
@@ -441,13 +385,13 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
     const int t2l1 = tid % TB, a1 = tid / TB;
     const bool act1 = a1 < P;
     float2 v[Q];
-    float2* tr = TDG_B_SEP_TR ? trb : sl;   // transposed tile: own region, or in place
+    float2* tr = sl;   // transposed in place
     if (act1) {
 #pragma unroll
         for (int b = 0; b < Q; ++b) v[b] = sl[(a1 + P * b) * TB + t2l1];
         dft<Q, +1>(v);
     }
-    if (!TDG_B_SEP_TR) __syncthreads();   // in place: every input read before any transposed write
+    __syncthreads();   // in place: every input read before any transposed write
     if (act1) {
 #pragma unroll
         for (int c = 0; c < Q; ++c) tr[a1 * ROW + c * TB + t2l1] = v[c];
@@ -463,12 +407,7 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
     if (c < Q) {
 #pragma unroll
         for (int a = 0; a < P; ++a) w[a] = tr[a * ROW + c * TB + t2l];
-        if (TDG_B_TW_SMEM) {
-#pragma unroll
-            for (int a = 1; a < P; ++a) w[a] = cmul(w[a], twb[a * Q + c]);
-        } else {
-            apply_step2_twiddles_anc<P, Q>(w, anc, c);
-        }
+        apply_step2_twiddles_anc<P, Q>(w, anc, c);
         dft<P, +1>(w);
         if (F::PFA) {
             // column t2 = t_b1 + QA t_a; outputs e are lags
@@ -476,13 +415,17 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
             constexpr uint32_t NN = uint32_t(F::LA) * uint32_t(F::LB), SE = NN / P;
             constexpr uint32_t NBB = NN / PA;
             const uint32_t tb1 = uint32_t(t2) % uint32_t(QA), ta = uint32_t(t2) / uint32_t(QA);
-            pfa_base = uint32_t((uint64_t(NBB) * ta + uint64_t(PA) * (tb1 + uint32_t(QA) * uint32_t(c))) % NN);
-            // valid lags t < W: e < e1 (before the wrap at e_w) and e in [e_w, e2)
-            const uint32_t e_w = (NN - pfa_base + SE - 1) / SE;
-            const uint32_t e_1 = W > pfa_base ? min(e_w, (W - pfa_base + SE - 1) / SE) : 0u;
-            const uint32_t e_2 = min(uint32_t(P), uint32_t((uint64_t(W) + NN - pfa_base + SE - 1) / SE));
-            auto low = [](uint32_t k) { return k >= 32u ? 0xffffffffu : (1u << k) - 1u; };
-            pfa_mask = low(e_1) | (e_2 > e_w ? low(e_2) & ~low(e_w) : 0u);
+            // (N/PA) t_a < N and PA (t_b1 + QA c) < PA QA QB <= N: one conditional subtract
+            pfa_base = NBB * ta + uint32_t(PA) * (tb1 + uint32_t(QA) * uint32_t(c));
+            pfa_base = pfa_base >= NN ? pfa_base - NN : pfa_base;
+            // t(e) = r + ((q + e) mod P) SE with base = q SE + r: valid iff
+            // (q + e) mod P < m = ceil((W - r) / SE); P == 32, so the valid-e mask
+            // is the low-m-bits mask rotated right by q
+            static_assert(!F::PFA || P == 32, "PFA lag mask assumes a 32-point last stage");
+            const uint32_t q = pfa_base / SE, r = pfa_base - q * SE;
+            const uint32_t m = W > r ? min(32u, (W - r + SE - 1) / SE) : 0u;
+            const uint32_t lowm = m >= 32u ? 0xffffffffu : (1u << m) - 1u;
+            pfa_mask = __funnelshift_r(lowm, lowm, q);
             if (S.write_xc) {
 #pragma unroll
                 for (int e = 0; e < P; ++e) {
@@ -616,37 +559,33 @@ template <int PA, int QA, int PB, int QB, int TYPE>
 __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_constant__ CorrSched S) {
     using F = Fused<PA, QA, PB, QB>;
     extern __shared__ __align__(128) unsigned char smraw[];
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smraw);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smraw);   // [0..1]: slot full
     float2* slots = reinterpret_cast<float2*>(smraw + 128);
-    float2* trb = slots + size_t(kSlots) * F::SLOT;   // pass B: separate transpose region (TDG_B_SEP_TR)
-    float2* twb = trb + F::B_TR;                      // pass B: twiddle table (TDG_B_TW_SMEM)
-    float2* anc = twb + F::B_TW;                      // step-2 twiddle anchors of this pass
+    float2* anc = slots + size_t(kSlots) * F::SLOT;      // step-2 twiddle anchors of this pass
     // the wave's descriptors live in shared memory (read by every item)
     unsigned char* dsm = smraw + F::SMEM;
     const int n_items = TYPE == 0 ? S.nA : S.nB;
+    const int den = TYPE == 0 ? S.ngw : S.n_tiles;
     const int i0 = int(int64_t(blockIdx.x) * n_items / gridDim.x);
     const int i1 = int(int64_t(blockIdx.x + 1) * n_items / gridDim.x);
-    // thread 0 starts the first item's bulk copies from the global descriptors
-    // while the CTA stages the descriptors in shared memory
-    constexpr bool SPLIT = TYPE == 0 && TDG_A_SPLIT && !TDG_A_PIPE && kSlots == 2;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // pass A: every warp's lane 0 issues its share of an item's bulk copies
+    // (issue_passA_role), so the slot barriers count NT/32 arrivals; pass B:
+    // thread 0 issues the tile
     if (threadIdx.x == 0) {
-        mbar_init(&bar[0], SPLIT ? F::NT / 32 : 1);
-        mbar_init(&bar[1], SPLIT ? F::NT / 32 : 1);
-        mbar_init(&bar[2], F::NT / 32);
-        mbar_init(&bar[3], F::NT / 32);
+        mbar_init(&bar[0], TYPE == 0 ? F::NT / 32 : 1);
+        mbar_init(&bar[1], TYPE == 0 ? F::NT / 32 : 1);
         mbar_fence_init();
-        if (!SPLIT && i0 < i1) {
-            const Desc Dg{S.groups, S.outs};
-            const Ticket k0{TYPE, 0, i0};
-            if (!ticket_noop(S, Dg, k0)) issue_ticket<PA, QA, PB, QB>(S, Dg, k0, slots, &bar[0]);
-        }
     }
-    if (SPLIT) {
-        __syncthreads();   // barriers initialised before any warp arrives on them
-        if ((threadIdx.x & 31) == 0 && i0 < i1) {
-            const Desc Dg{S.groups, S.outs};
-            const Ticket k0{TYPE, 0, i0};
-            if (!ticket_noop(S, Dg, k0)) issue_passA_role<PA, QA, PB, QB>(S, Dg, k0, slots, &bar[0], threadIdx.x >> 5);
+    if (TYPE == 0) __syncthreads();   // barriers initialised before any warp arrives on them
+    // the first item's bulk copies from the global descriptors, while the CTA
+    // stages the descriptors in shared memory
+    if (i0 < i1) {
+        const Desc Dg{S.groups, S.outs};
+        const Ticket k0 = ticket_at(i0, den);
+        if (!ticket_noop<TYPE>(Dg, k0)) {
+            if (TYPE == 0 && lane == 0) issue_passA_role<PA, QA, PB, QB>(S, Dg, k0, slots, &bar[0], warp);
+            if (TYPE == 1 && threadIdx.x == 0) issue_tile<PA, QA, PB, QB>(Dg, k0, slots, &bar[0]);
         }
     }
     Desc D;
@@ -662,93 +601,33 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
         D.groups = reinterpret_cast<const CorrGroup<kGroup>*>(dsm);
         D.outs = reinterpret_cast<const CorrPairOut*>(dsm + nb_g);
     }
-    if (TYPE == 1 && TDG_B_TW_SMEM)
-        for (int i = threadIdx.x; i < F::LB; i += F::NT) twb[i] = __ldg(&S.twB[i]);
     if (TYPE == 1)
         fill_twiddle_anchors<PB, QB>(anc, S.twB, threadIdx.x, F::NT);
     else if (!F::PFA)
         fill_twiddle_anchors<PA, QA>(anc, S.twA, threadIdx.x, F::NT);
     __syncthreads();
-    if (TYPE == 0 && TDG_A_PIPE && kSlots == 2) {
-        // bar[0..1]: slot full (TMA bytes); bar[2..3]: slot released by all
-        // four warps.  Item j lives in slot j & 1; during item j (after step
-        // 1) every warp releases the slot of item j - 1 and thread 0 refills
-        // it with item j + 1.  No CTA-wide barrier inside the loop.
-        uint64_t* empty = bar + 2;
-        uint32_t full_ph = 0u, empty_ph = 0u;
-        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        for (int item = i0, j = 0; item < i1; ++item, ++j) {
-            const int s = j & 1;
-            auto refill = [&]() {
-                if (item + 1 >= i1) return;
-                const int t = s ^ 1;   // slot of item j - 1, to hold item j + 1
-                if (j >= 1) {
-                    if (lane == 0) {
-                        bulk_wait_read_all();   // this warp's store of item j - 1 has read its staging
-                        mbar_arrive(&empty[t]);
-                    }
-                    if (threadIdx.x == 0) {
-                        mbar_wait(&empty[t], (empty_ph >> t) & 1u);
-                    }
-                    empty_ph ^= 1u << t;
-                }
-                if (threadIdx.x == 0) {
-                    const Ticket kn{TYPE, 0, item + 1};
-                    if (!ticket_noop(S, D, kn))
-                        issue_ticket<PA, QA, PB, QB>(S, D, kn, slots + size_t(t) * F::SLOT, &bar[t]);
-                }
-            };
-            const Ticket k{TYPE, 0, item};
-            if (ticket_noop(S, D, k)) {
-                refill();
-                continue;
-            }
-            float2* sl = slots + size_t(s) * F::SLOT;
-            mbar_wait(&bar[s], (full_ph >> s) & 1u);
-            full_ph ^= 1u << s;
-            item_passA<PA, QA, PB, QB>(S, D, k, sl, refill, anc);
-            __syncwarp();
-            if (lane == 0) store_passA_role<PA, QA, PB, QB>(S, D, k, sl, warp);
-        }
-        if (lane == 0) bulk_wait_all();
-        return;
-    }
     uint32_t phases = 0u;   // bit s: parity of slot s's mbarrier
-    for (int item = i0, s = 0; item < i1; ++item, s ^= (kSlots - 1)) {
-        // next item's bulk copies into slot s^1 (two slots): pass B at the
-        // top of the item; pass A halfway through (after step 1), once the
-        // TMA stores of the item that last used slot s^1 have read their
-        // staging area.  One slot: after this item (below).
+    Ticket k = ticket_at(i0, den);
+    for (int item = i0, s = 0; item < i1; ++item, s ^= 1) {
+        Ticket kn = k;
+        ticket_next(kn, den);
+        // the next item's bulk copies into slot s^1: pass B at the top of the
+        // item; pass A halfway through (after step 1), each warp once its TMA
+        // store of the item that last used slot s^1 has read its staging area
         auto prefetch = [&]() {
-            if (SPLIT) {
-                if ((threadIdx.x & 31) == 0 && item + 1 < i1) {
-                    bulk_wait_read_all();   // this warp's store of the slot's last item has read it
-                    const Ticket kn{TYPE, 0, item + 1};
-                    if (!ticket_noop(S, D, kn))
-                        issue_passA_role<PA, QA, PB, QB>(S, D, kn, slots + size_t(s ^ 1) * F::SLOT, &bar[s ^ 1],
-                                                         threadIdx.x >> 5);
-                }
-                return;
+            if (item + 1 >= i1) return;
+            if (TYPE == 0 && lane == 0) {
+                bulk_wait_read_all();
+                if (!ticket_noop<TYPE>(D, kn))
+                    issue_passA_role<PA, QA, PB, QB>(S, D, kn, slots + size_t(s ^ 1) * F::SLOT, &bar[s ^ 1], warp);
             }
-            if (kSlots == 2 && threadIdx.x == 0 && item + 1 < i1) {
-                if (TYPE == 0) bulk_wait_read_all();
-                const Ticket kn{TYPE, 0, item + 1};
-                if (!ticket_noop(S, D, kn))
-                    issue_ticket<PA, QA, PB, QB>(S, D, kn, slots + size_t(s ^ 1) * F::SLOT, &bar[s ^ 1]);
-            }
-        };
-        auto prefetch_after = [&]() {
-            if (kSlots == 1 && threadIdx.x == 0 && item + 1 < i1) {
-                if (TYPE == 0) bulk_wait_read_all();
-                const Ticket kn{TYPE, 0, item + 1};
-                if (!ticket_noop(S, D, kn)) issue_ticket<PA, QA, PB, QB>(S, D, kn, slots, &bar[0]);
-            }
+            if (TYPE == 1 && threadIdx.x == 0 && !ticket_noop<TYPE>(D, kn))
+                issue_tile<PA, QA, PB, QB>(D, kn, slots + size_t(s ^ 1) * F::SLOT, &bar[s ^ 1]);
         };
         if (TYPE == 1) prefetch();
-        const Ticket k{TYPE, 0, item};
-        if (ticket_noop(S, D, k)) {
+        if (ticket_noop<TYPE>(D, k)) {
             if (TYPE == 0) prefetch();
-            prefetch_after();
+            k = kn;
             continue;
         }
         float2* sl = slots + size_t(s) * F::SLOT;
@@ -762,24 +641,20 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
             // tile: a tile that does not start on a 128-byte line (N1 * 32
             // bytes not a multiple of 128, e.g. N1 = 450) shares its edge lines
             // with the neighbouring tiles, whose items may not have read them yet.
-            const CorrPairOut& po = D.outs[k.idx / S.n_tiles];
-            const uintptr_t t0 = reinterpret_cast<uintptr_t>(po.M + size_t(k.idx % S.n_tiles) * F::LB * kTileB);
+            const CorrPairOut& po = D.outs[k.u];
+            const uintptr_t t0 = reinterpret_cast<uintptr_t>(po.M + size_t(k.v) * F::LB * kTileB);
             const uintptr_t lo = (t0 + 127) & ~uintptr_t(127);
             const uintptr_t hi = (t0 + uintptr_t(F::LB) * kTileB * 8) & ~uintptr_t(127);
             if (S.discard)
                 for (uintptr_t a = lo + uintptr_t(threadIdx.x) * 128; a < hi; a += uintptr_t(F::NT) * 128)
                     discard_l2(reinterpret_cast<const void*>(a));
-            item_passB<PA, QA, PB, QB>(S, D, k, sl, trb, twb, anc);
+            item_passB<PA, QA, PB, QB>(S, D, k, sl, anc);
         }
         __syncthreads();   // slot s consumed (pass A: its staged columns complete)
-        if (SPLIT) {
-            if ((threadIdx.x & 31) == 0) store_passA_role<PA, QA, PB, QB>(S, D, k, sl, threadIdx.x >> 5);
-        } else if (TYPE == 0 && threadIdx.x == 0) {
-            store_passA<PA, QA, PB, QB>(S, D, k, sl);
-        }
-        prefetch_after();
+        if (TYPE == 0 && lane == 0) store_passA_role<PA, QA, PB, QB>(S, D, k, sl, warp);
+        k = kn;
     }
-    if (TYPE == 0 && (SPLIT ? (threadIdx.x & 31) == 0 : threadIdx.x == 0)) bulk_wait_all();
+    if (TYPE == 0 && lane == 0) bulk_wait_all();
 }
 
 }  // namespace tdg

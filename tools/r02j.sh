@@ -1,0 +1,5 @@
+OUT=gpurun_out/${TAG:-r02j}; mkdir -p $OUT
+./tools/microbench/mix > $OUT/mix.txt 2>&1
+ncu --metrics smsp__inst_executed_op_shared_st.sum,smsp__inst_executed_op_global_st.sum,smsp__inst_executed.sum -k regex:kmix --csv ./tools/microbench/mix > $OUT/mix_ncu.csv 2>&1
+timeout 600 ncu --set full --warp-sampling-interval 0 --warp-sampling-max-passes 20 --warp-sampling-buffer-size 268435456 --clock-control none --import-source on -k regex:k_corr_pass --profile-from-start off -s 4 -c 2 -o $OUT/full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --profile-step > $OUT/ncu.log 2>&1
+nvidia-smi > $OUT/smi_end.txt 2>&1
