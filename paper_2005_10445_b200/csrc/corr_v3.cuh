@@ -654,7 +654,10 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
         if (TYPE == 0 && lane == 0) store_passA_role<PA, QA, PB, QB>(S, D, k, sl, warp);
         k = kn;
     }
-    if (TYPE == 0 && lane == 0) bulk_wait_all();
+    // the CTA's shared memory must outlive the reads of its last TMA stores;
+    // the stores' global writes are complete by the end of the grid (what
+    // orders pass B after them), so only the reads are waited for here
+    if (TYPE == 0 && lane == 0) bulk_wait_read_all();
 }
 
 }  // namespace tdg
