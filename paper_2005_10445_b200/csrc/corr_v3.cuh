@@ -111,7 +111,7 @@ struct CorrSched {                     // one wave
     int ngw, wave_pairs, n_tiles, nA, nB, N1, N2;
     int write_xc;                      // 1: full xc rows (batch_xcorr), 0: argmax keys
     int discard;                       // 1: drop consumed M tiles from L2 (no write-back)
-    uint32_t W;
+    uint32_t W;                        // window length (lag limits are per pair: CorrPairOut)
     float inv_n;
 };
 
@@ -380,7 +380,7 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
         cur_a = __uint_as_float(uint32_t(ld_relaxed_u64(po.key_a) >> 32));
         if (po.key_b) cur_b = __uint_as_float(uint32_t(ld_relaxed_u64(po.key_b) >> 32));
     }
-    const uint32_t W = S.W;
+    const uint32_t W = po.lag_lim;   // valid local lags [0, W)
     // step 1: task (a, t2l), t2l fastest
     const int t2l1 = tid % TB, a1 = tid / TB;
     const bool act1 = a1 < P;
@@ -508,8 +508,8 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
                     }
                 }
             }
-            unsigned long long ka = need_a && ta != 0xffffffffu ? peak_key(best_a, ta) : 0ull;
-            unsigned long long kb = need_b && tb != 0xffffffffu ? peak_key(best_b, tb) : 0ull;
+            unsigned long long ka = need_a && ta != 0xffffffffu ? peak_key(best_a, po.lag0 + ta) : 0ull;
+            unsigned long long kb = need_b && tb != 0xffffffffu ? peak_key(best_b, po.lag0 + tb) : 0ull;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 const unsigned long long xa = __shfl_xor_sync(0xffffffffu, ka, o);
@@ -533,9 +533,9 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
                 }
             }
             unsigned long long ka = need_a && ea < P
-                ? peak_key(best_a, uint32_t(t2) + uint32_t(N2) * uint32_t(c + Q * ea)) : 0ull;
+                ? peak_key(best_a, po.lag0 + uint32_t(t2) + uint32_t(N2) * uint32_t(c + Q * ea)) : 0ull;
             unsigned long long kb = need_b && eb < P
-                ? peak_key(best_b, uint32_t(t2) + uint32_t(N2) * uint32_t(c + Q * eb)) : 0ull;
+                ? peak_key(best_b, po.lag0 + uint32_t(t2) + uint32_t(N2) * uint32_t(c + Q * eb)) : 0ull;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 const unsigned long long xa = __shfl_xor_sync(0xffffffffu, ka, o);

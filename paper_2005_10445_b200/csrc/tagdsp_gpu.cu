@@ -792,6 +792,16 @@ struct tdg_codeset {
     std::vector<uint64_t> nlen;
     std::vector<float> energy, abs_sum;
     uint64_t corr_len() const { return uint64_t(N1) * uint64_t(N2); }
+    // Segmented correlation (windows longer than the largest transform,
+    // N = 1024 x 1024): seg_lags > 0 splits a window's lags [0, W) into
+    // segments of seg_lags lags; segment g correlates d[g*B, g*B + B + nmax - 1)
+    // (B = seg_lags, nmax = the longest support), which a transform of
+    // N >= B + nmax - 1 holds without wrap-around, and its argmax keys merge
+    // into the window's (atomicMax over the global lag).  0 = one transform
+    // per window.
+    uint64_t seg_lags = 0;
+    uint64_t nmax = 0;
+    uint64_t n_segments(uint64_t W) const { return seg_lags ? (W + seg_lags - 1) / seg_lags : 1; }
 };
 
 struct tdg_windows {
@@ -800,8 +810,9 @@ struct tdg_windows {
     uint64_t W = 0, n_windows = 0, n_bins = 0;
     DevBuf d, u;
     std::vector<int64_t> start;   // window_start per slot
-    DevBuf dspec;
+    DevBuf dspec;                 // [slot][segment] half-column spectra
     uint64_t dspec_N = 0;         // transform length dspec was computed for (0 = stale)
+    uint64_t dspec_seg = 0;       // ... and its segment length (codeset seg_lags, nmax)
     uint64_t active = 0;          // slots in use (tracking batches reuse a larger set); 0 = all
     uint64_t slots() const { return n_windows * n_bins; }
     uint64_t used() const { return active ? active : slots(); }
@@ -927,36 +938,53 @@ void run_forward(tdg_ctx* ctx, int N1, int N2, const std::vector<FwdJob>& jobs, 
     }
 }
 
-// Window spectra of every used slot.  slot_ready (optional) receives, per
-// forward-transform wave, (slots complete, event on the context stream) so
-// that correlations of early slots can start while later slots transform.
-void ensure_dspec(tdg_ctx* ctx, tdg_windows* w, int N1, int N2,
+// Window spectra of every used slot (and segment, cs->seg_lags).  slot_ready
+// (optional) receives, per forward-transform wave, (spectrum slots complete,
+// event on the context stream) so that correlations of early slots can start
+// while later slots transform.  Spectrum slot of (slot s, segment g) =
+// s * n_segments + g.
+void ensure_dspec(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs,
                   std::vector<std::pair<size_t, cudaEvent_t>>* slot_ready = nullptr) {
+    const int N1 = cs->N1, N2 = cs->N2;
     const uint64_t N = uint64_t(N1) * uint64_t(N2);
-    if (w->dspec_N == N) return;
+    const uint64_t seg_key = cs->seg_lags ? cs->seg_lags * (uint64_t(1) << 24) + cs->nmax : 0;
+    if (w->dspec_N == N && w->dspec_seg == seg_key) return;
     const uint64_t H = uint64_t(N1 / 2 + 1) * uint64_t(N2);
-    w->dspec.ensure(w->slots() * H * sizeof(float2));
+    const uint64_t nseg = cs->n_segments(w->W), nss = w->used() * nseg;
+    w->dspec.ensure(w->slots() * nseg * H * sizeof(float2));
+    auto seq = [&](uint64_t ss, const float** r, uint64_t* len) {
+        const uint64_t s = ss / nseg, g = ss % nseg;
+        const uint64_t o = g * cs->seg_lags;
+        *r = w->d.as<float>() + s * w->W + o;
+        *len = cs->seg_lags ? std::min(w->W - o, cs->seg_lags + cs->nmax - 1) : w->W;
+    };
     std::vector<FwdJob> jobs;
-    for (uint64_t s = 0; s < w->used(); s += 2) {
-        const bool two = s + 1 < w->used();
-        jobs.push_back({w->d.as<float>() + s * w->W, two ? w->d.as<float>() + (s + 1) * w->W : nullptr, w->W,
-                        two ? w->W : 0, w->dspec.as<float2>() + s * H, two ? w->dspec.as<float2>() + (s + 1) * H : nullptr});
+    for (uint64_t ss = 0; ss < nss; ss += 2) {
+        const bool two = ss + 1 < nss;
+        const float *r1 = nullptr, *r2 = nullptr;
+        uint64_t l1 = 0, l2 = 0;
+        seq(ss, &r1, &l1);
+        if (two) seq(ss + 1, &r2, &l2);
+        jobs.push_back({r1, r2, l1, l2, w->dspec.as<float2>() + ss * H, two ? w->dspec.as<float2>() + (ss + 1) * H : nullptr});
     }
     run_forward(ctx, N1, N2, jobs, true, slot_ready);
     if (slot_ready)
-        for (auto& c : *slot_ready) c.first = std::min<size_t>(2 * c.first, w->used());   // pair jobs -> slots
+        for (auto& c : *slot_ready) c.first = std::min<size_t>(2 * c.first, nss);   // pair jobs -> spectrum slots
     w->dspec_N = N;
+    w->dspec_seg = seg_key;
 }
 
 // Correlation jobs: each is one stored code pair (codes 2p, 2p+1) against
 // one window slot; outputs are argmax keys and/or full xc rows.
 struct CorrJob {
-    uint64_t slot;
+    uint64_t slot;               // spectrum slot (window slot * n_segments + segment)
     uint64_t pair;
     unsigned long long* key_a;
     unsigned long long* key_b;   // nullptr if the pair has one code
-    float* xc_a;                 // diagnostic outputs (nullable)
+    float* xc_a;                 // diagnostic outputs (nullable), at the segment's first lag
     float* xc_b;
+    uint32_t lag0 = 0;           // global lag of the segment's local lag 0
+    uint32_t lag_lim = 0;        // local lags [0, lag_lim); 0 = the window length
 };
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
@@ -1028,7 +1056,7 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
     const uint64_t N = cs->corr_len(), H = cs->H;
     // allocate the window spectra now (their addresses go into the
     // descriptors); the transforms themselves are enqueued after the fork
-    w->dspec.ensure(w->slots() * H * sizeof(float2));
+    w->dspec.ensure(w->slots() * cs->n_segments(w->W) * H * sizeof(float2));
     constexpr int G = tdg::kGroup;
     const int wave = int(std::max<int64_t>(G, ctx->wave_pairs / G * G));
     const int n_waves = int((jobs.size() + size_t(wave) - 1) / size_t(wave));
@@ -1070,6 +1098,8 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
             o.key_b = jb.key_b;
             o.xc_a = jb.xc_a;
             o.xc_b = jb.xc_b;
+            o.lag0 = jb.lag0;
+            o.lag_lim = jb.lag_lim ? jb.lag_lim : uint32_t(w->W);
         }
     }
     ctx->pk->corr.begin();
@@ -1098,7 +1128,7 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
         // one wave (small tracking batches): nothing to overlap, so no fork,
         // events or join -- the transforms and both passes in order on the
         // context stream (API calls are most of a small batch's latency)
-        ensure_dspec(ctx, w, N1, N2);
+        ensure_dspec(ctx, w, cs);
         S.groups = gd;
         S.outs = od;
         launch_pass<0>(N1, N2, ctx->stream, S, ctx->cta_cap[0]);
@@ -1118,7 +1148,7 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
         CK(cudaStreamWaitEvent(ctx->b_streams[size_t(i)], ctx->ev_fork, 0));
     }
     std::vector<std::pair<size_t, cudaEvent_t>> ready;   // (slots transformed, event)
-    ensure_dspec(ctx, w, N1, N2, &ready);
+    ensure_dspec(ctx, w, cs, &ready);
     std::vector<size_t> waited(size_t(ns), 0);            // ready[] prefix each A stream has waited for
     for (int wv = 0; wv < n_waves; ++wv) {
         const int r = wv % ring;
@@ -1333,14 +1363,23 @@ void append_codes(tdg_ctx* ctx, tdg_codeset* cs, const float* d, const float* u,
     }
     if (cs->window_len >= (uint64_t(1) << 32)) fail(TDG_ERANGE, "window_len too large");
     int N1 = 0, N2 = 0;
+    uint64_t seg_lags = 0;
     if (!choose_corr_len(cs->window_len + nmax - 1, &N1, &N2)) {
-        cs->nlen.resize(n0);
-        cs->energy.resize(n0);
-        cs->abs_sum.resize(n0);
-        fail(TDG_ERANGE, "window_len + support %llu exceeds the largest supported transform",
-             (unsigned long long)(cs->window_len + nmax));
+        // longer than one transform: segmented correlation with the largest
+        // split, each segment's lags [gB, gB + B) from B + nmax - 1 samples
+        N1 = N2 = 1024;
+        const uint64_t Nmax = uint64_t(N1) * uint64_t(N2);
+        if (nmax > Nmax / 2) {
+            cs->nlen.resize(n0);
+            cs->energy.resize(n0);
+            cs->abs_sum.resize(n0);
+            fail(TDG_ERANGE, "code support %llu exceeds half of the largest transform", (unsigned long long)nmax);
+        }
+        seg_lags = Nmax - nmax + 1;
     }
     cs->n_codes = nt;
+    cs->seg_lags = seg_lags;
+    cs->nmax = nmax;
     const bool relen = N1 != cs->N1 || N2 != cs->N2;
     cs->N1 = N1;
     cs->N2 = N2;
@@ -1675,9 +1714,11 @@ void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float thre
     std::vector<char> want_pair((nc + 1) / 2, 0);
     for (uint64_t c : *sel) {
         if (c >= nc) fail(TDG_EINVAL, "detect: code index out of range");
-        if (w->W + cs->nlen[c] > cs->corr_len() + 1) fail(TDG_EINVAL, "batch_xcorr: window does not fit transform size");
+        if (!cs->seg_lags && w->W + cs->nlen[c] > cs->corr_len() + 1)
+            fail(TDG_EINVAL, "batch_xcorr: window does not fit transform size");
         want_pair[c / 2] = 1;
     }
+    const uint64_t nseg = cs->n_segments(w->W);
     if (!nk) return;
     // argmax keys [slot][code] of every code of a touched pair (the packed
     // IFFT yields both codes of a pair)
@@ -1692,11 +1733,16 @@ void detect_impl(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, float thre
         if (want_pair[p]) pairs.push_back(p);
     const uint64_t G = tdg::kGroup;
     for (uint64_t i0 = 0; i0 < pairs.size(); i0 += G) {
-        for (uint64_t s = 0; s < ns; ++s)
+        for (uint64_t ss = 0; ss < ns * nseg; ++ss)
             for (uint64_t i = i0; i < std::min<uint64_t>(pairs.size(), i0 + G); ++i) {
-                const uint64_t p = pairs[i];
-                jobs.push_back({s, p, keys + s * nc + 2 * p, 2 * p + 1 < nc ? keys + s * nc + 2 * p + 1 : nullptr,
-                                nullptr, nullptr});
+                const uint64_t p = pairs[i], s = ss / nseg, g = ss % nseg;
+                CorrJob jb{ss, p, keys + s * nc + 2 * p, 2 * p + 1 < nc ? keys + s * nc + 2 * p + 1 : nullptr,
+                           nullptr, nullptr};
+                if (cs->seg_lags) {
+                    jb.lag0 = uint32_t(g * cs->seg_lags);
+                    jb.lag_lim = uint32_t(std::min(cs->seg_lags, w->W - g * cs->seg_lags));
+                }
+                jobs.push_back(jb);
             }
     }
     ctx->det_dev.ensure(ns * nk * sizeof(tdg_detection));
@@ -1802,7 +1848,18 @@ int tdg_batch_xcorr(tdg_ctx* ctx, tdg_windows* w, uint64_t slot, const tdg_codes
             (c % 2 ? pp.second : pp.first) = xc.as<float>() + r * w->W;
         }
         std::vector<CorrJob> jobs;
-        for (auto& [p, rows] : per_pair) jobs.push_back({slot, p, nullptr, nullptr, rows.first, rows.second});
+        const uint64_t nseg = cs->n_segments(w->W);
+        for (uint64_t g = 0; g < nseg; ++g)
+            for (auto& [p, rows] : per_pair) {
+                const uint64_t o = g * cs->seg_lags;
+                CorrJob jb{slot * nseg + g, p, nullptr, nullptr, rows.first ? rows.first + o : nullptr,
+                           rows.second ? rows.second + o : nullptr};
+                if (cs->seg_lags) {
+                    jb.lag0 = uint32_t(o);
+                    jb.lag_lim = uint32_t(std::min(cs->seg_lags, w->W - o));
+                }
+                jobs.push_back(jb);
+            }
         run_correlations(ctx, w, cs, jobs, true);
         for (uint64_t i = 0; i < n_idx; ++i)
             CK(cudaMemcpyAsync(out + i * w->W, xc.as<float>() + row_of[uint64_t(codes[i])] * w->W,
@@ -1850,6 +1907,8 @@ namespace {
 void track_impl(tdg_ctx* ctx, const tdg_demod_config* cfg, const SampleSource& src, const tdg_track_task* tasks,
                 uint64_t n_tasks, const tdg_codeset* cs, float threshold, tdg_detection* out, bool sync = true) {
     const uint64_t W = cs->window_len;
+    if (cs->seg_lags)
+        fail(TDG_ERANGE, "track: windows longer than one transform (segmented code sets) are searched, not tracked");
     for (uint64_t i = 0; i < n_tasks; ++i) {
         if (tasks[i].code_index >= cs->n_codes) fail(TDG_EINVAL, "track: task %llu code index out of range",
                                                      (unsigned long long)i);

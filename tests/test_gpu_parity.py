@@ -324,10 +324,12 @@ def test_invalid_arguments_raise(gpu_ctx):
         capi.detect(gpu_ctx, w, cs)                               # mixed window shapes
     with pytest.raises(capi.InvalidArgument):
         capi.demodulate_window(gpu_ctx, np.zeros(3, np.int16), 0, cfg)   # odd raw count
-    # beyond the largest instantiated transform (1024 x 1024): a clear error, no launch
+    # beyond one transform (1024 x 1024) the window is correlated in segments
+    # (tests below); a support longer than half the largest transform is
+    # rejected with a clear error, before any launch
     assert capi.corr_len(1 << 20, 2) == 0
-    with pytest.raises(capi.GpuError, match="largest supported transform"):
-        capi.CodeSet.from_replicas(gpu_ctx, 1 << 20, (1 << 20) + 100, [np.ones(64, np.float32)])
+    with pytest.raises(capi.GpuError, match="half of the largest transform"):
+        capi.CodeSet.from_replicas(gpu_ctx, 1 << 21, (1 << 21) + 600000, [np.ones(600000, np.float32)])
 
 
 def test_tracking_batch_parity(gpu_ctx, ref):
@@ -460,3 +462,55 @@ def test_tracking_rejects_bad_tasks(gpu_ctx):
     with pytest.raises(capi.InvalidArgument):
         capi.track(gpu_ctx, cfg, iq, [0], [2], cs)            # code index out of range
     assert capi.track(gpu_ctx, cfg, iq, [], [], cs).size == 0
+
+
+def _scene_two_codes(ref, cfg, bits, W, delays, seed):
+    a = ref.channel_window(bits[0], cfg, delays[0], W, seed, snr_db=5.0).astype(np.int32)
+    b = ref.channel_window(bits[1], cfg, delays[1], W, seed + 1, snr_db=5.0).astype(np.int32)
+    return np.clip(a + b, -32767, 32767).astype(np.int16)
+
+
+@pytest.mark.parametrize("W", [300000, 1200000])
+def test_window_lengths_beyond_the_menu(gpu_ctx, ref, W):
+    """Any W the reference's pad_length accepts (proj/src/fft.cpp:93-101,
+    detector.hpp:19-21): W = 300,000 lies between the instantiated splits
+    (padded up to the next one), W = 1,200,000 (150 ms at 8 Ms/s) needs
+    W + n - 1 > 1024 x 1024 and runs as a segmented correlation -- segments of
+    B = 2^20 - n + 1 lags, each from B + n - 1 samples, argmax keys merged over
+    the global lag.  Code 1 sits across the segment boundary (its peak lag
+    within a few samples of B), code 0 early; every Detection field is checked
+    against the reference compiled in place, and batch_xcorr's full rows too."""
+    from paper_2005_10445_b200 import capi
+    from paper_2005_10445_b200._abi import demod_config
+    cfg = demod_config()
+    bits = np.stack([ref.gen_code(2000 + i, cfg) for i in range(4)])
+    cs = capi.CodeSet.prepare(gpu_ctx, cfg, W, bits)
+    n = max(cs.info(i)["nonzero_len"] for i in range(len(bits)))
+    B = (1 << 20) - n + 1
+    seg = W + n - 1 > (1 << 20)
+    delays = (1000.25, (B - 3.5) if seg else W // 2 + 0.5)
+    iq = _scene_two_codes(ref, cfg, bits, W, delays, 41)
+    win = capi.Windows(gpu_ctx, W)
+    win.demodulate(cfg, [0.0], iq, 0, W, 1)
+    dets = capi.detect(gpu_ctx, win, cs, 0.25, cfg.mod.sample_rate)
+    s = ref.Session()
+    idx = [s.prepare_code(bits[i], cfg, W, "c%d" % i) for i in range(len(bits))]
+    d, u = ref.demodulate_window(iq, 0, cfg)
+    want = s.detect(d, u, idx, 0.25, 0, cfg.mod.sample_rate)
+    assert want[0]["accepted"] and want[1]["accepted"]
+    assert abs(int(want[1]["peak_index"]) - int(delays[1])) <= 2
+    xc = s.batch_xcorr(d, idx)
+
+    def tie_ok(g, w):
+        c = int(w["code_index"])
+        return near_tie_margin(xc[c], int(w["peak_index"]), int(g["peak_index"])) < 1e-5
+
+    bad = compare_detections(dets, want, cfg.mod.sample_rate, tie_ok=tie_ok, xc_ref=xc, eps=1e-5,
+                             pc_ref=(u, {i: s.code_replica(idx[i]) for i in range(len(bits))}))
+    assert not bad, bad
+    # full correlation rows, segment by segment, against the reference's
+    win.set_du(0, d, u)
+    got = capi.batch_xcorr(gpu_ctx, win, 0, cs)
+    for i in range(len(bits)):
+        e = cs.info(i)["energy"]
+        assert np.abs(got[i] - xc[i]).max() <= 2e-5 * e, i
