@@ -28,6 +28,18 @@ ncu)
   true ;;
 track)
   timeout 600 python bench.py --workload tracking > $OUT/track.json 2> $OUT/track.err; echo "track rc=$?" >> $OUT/track.err ;;
+roster)
+  timeout 600 python bench.py --workload roster --no-cpu-baseline > $OUT/roster.json 2> $OUT/roster.err; echo "roster rc=$?" >> $OUT/roster.err ;;
+streams)
+  timeout 600 python bench.py --workload streams --no-cpu-baseline > $OUT/streams.json 2> $OUT/streams.err; echo "streams rc=$?" >> $OUT/streams.err ;;
+reference)
+  timeout 900 python bench.py --impl reference > $OUT/ref.json 2> $OUT/ref.err; echo "ref rc=$?" >> $OUT/ref.err ;;
+full)
+  timeout 900 ncu --set full --warp-sampling-interval 0 --warp-sampling-max-passes 20 --warp-sampling-buffer-size 268435456 --clock-control none --import-source on -k regex:k_corr_pass --profile-from-start off -s 4 -c 2 \
+      -o $OUT/full python bench.py --steps 1 --warmup 3 --no-cpu-baseline --profile-step > $OUT/ncu_full.log 2>&1
+  true ;;
+smi)
+  nvidia-smi > $OUT/smi_end.txt 2>&1 ;;
 sweep)
   timeout 600 python tools/sweep.py $SWEEP > $OUT/sweep.log 2>&1 ;;
 esac
