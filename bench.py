@@ -607,6 +607,18 @@ def main():
     wall_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / args.steps)
     e2e = n_units * world / (e2e_ms / 1e3)
 
+    # ---- GPU code preparation (prepare_code for the whole
+    # set -- synth_replica, demodulation, support/energy, forward transforms of
+    # the code pairs), a fresh set of the same codes, outside the timed steps
+    barrier()
+    t_prep = time.perf_counter()
+    cs2 = capi.CodeSet.prepare(ctx, cfg, W, bits)
+    ctx.synchronize()
+    prep_ms = (time.perf_counter() - t_prep) * 1e3
+    cs2.close()
+    code_prep = {"codes": n_codes, "ms": round(prep_ms, 3), "codes_per_s": round(n_codes / (prep_ms / 1e3), 1),
+                 "note": "wall clock of one tdg_codeset_prepare (synchronous), window_len %d" % W}
+
     # ---- per-kernel CUDA events (same steps, separate pass: recording an
     # event pair around each of ~800 launches perturbs the step time) -------
     ctx.kernel_time_reset()
@@ -673,6 +685,7 @@ def main():
                         "stream) + tdg_search_ring (Detection records -> pinned host), upload of step k+1 "
                         "overlapping the search of step k"},
         "gpu_launches": int(launches),
+        "code_prep": code_prep,
         "roofline": dict(roof, **{
             "kernel": "correlation engine per step: k_corr_pass<27,32,32,32,0> (spectral product + first "
                       "inverse-FFT pass) and k_corr_pass<...,1> (second pass + argmax) in waves over 6 pass-A + 6 "
