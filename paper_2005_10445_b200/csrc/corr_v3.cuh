@@ -94,7 +94,7 @@ struct Fused {
     static constexpr int SLOT = cmax(A_SLOT, B_SLOT);
     static constexpr int NT = 128;
     // slots, then (pass B) the transpose region and the twiddle table
-    static constexpr int ANC = 4 * cmax(QA, QB);                             // step-2 twiddle anchors
+    static constexpr int ANC = 5 * cmax(QA, QB);   // step-2 twiddle anchors (+ pass B PFA: w_32^{-q})
     static constexpr size_t SMEM = 128 + kSlots * size_t(SLOT) * 8 + size_t(ANC) * 8;
     static_assert(cmax(PA, QA) <= 32 && cmax(PB, QB) <= 32, "one warp per column role");
     static_assert(LA % kTileB == 0, "M tiles cover the t2 columns exactly (TMA store box)");
@@ -135,6 +135,13 @@ __device__ __forceinline__ int tid_x() {
 // An item's coordinates: pass A (u, v) = (column pair cp, group), item
 // u * ngw + v; pass B (u, v) = (pair, M tile), item u * n_tiles + v.  A CTA
 // walks a contiguous item range, so they advance without divisions.
+// max(m, |x|, |y|) as one FMNMX3 (three-input max with |.| operand modifiers)
+__device__ __forceinline__ float fmax3_abs(float m, float x, float y) {
+    float d;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(m), "f"(fabsf(x)), "f"(fabsf(y)));
+    return d;
+}
+
 struct Ticket {
     int u, v;
 };
@@ -402,57 +409,92 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
     const int t2 = tb * TB + t2l;
     float best_a = -1.f, best_b = -1.f;
     int e_lim = 0;
-    uint32_t pfa_base = 0, pfa_mask = 0;   // PFA: lag of e = 0 and valid-e mask
+    uint32_t pfa_base = 0, pfa_m = 0;   // PFA: lag of slot 0 and valid slots e < pfa_m
     float2 w[P];
     if (c < Q) {
 #pragma unroll
         for (int a = 0; a < P; ++a) w[a] = tr[a * ROW + c * TB + t2l];
-        apply_step2_twiddles_anc<P, Q>(w, anc, c);
-        dft<P, +1>(w);
         if (F::PFA) {
-            // column t2 = t_b1 + QA t_a; outputs e are lags
-            // t = ((N/PA) t_a + PA (t_b1 + QA (c + Q e))) mod N = (base + e*SE) mod N
+            // column t2 = t_b1 + QA t_a; output e of the last DFT is the lag
+            // t = ((N/PA) t_a + PA (t_b1 + QA (c + Q e))) mod N = (base + e SE) mod N,
+            // base = q SE + r.  The step-2 twiddles are taken as
+            // w_L^{a (c - Q q)} instead of w_L^{a c} -- the extra w_P^{-a q} rotates
+            // the DFT's outputs so that slot e holds lag r + e SE: no wrap, the
+            // valid lags t < W are the prefix e < m = ceil((W - r) / SE), and the
+            // lags rise with e.  (anchors at a = 8j pick up a quarter turn
+            // i^{-jq}; the base twiddle one multiply by w_P^{-q})
+            static_assert(!F::PFA || (P == 32 && Q == 32), "rotated PFA epilogue assumes a 32 x 32 last pass");
             constexpr uint32_t NN = uint32_t(F::LA) * uint32_t(F::LB), SE = NN / P;
             constexpr uint32_t NBB = NN / PA;
             const uint32_t tb1 = uint32_t(t2) % uint32_t(QA), ta = uint32_t(t2) / uint32_t(QA);
             // (N/PA) t_a < N and PA (t_b1 + QA c) < PA QA QB <= N: one conditional subtract
-            pfa_base = NBB * ta + uint32_t(PA) * (tb1 + uint32_t(QA) * uint32_t(c));
-            pfa_base = pfa_base >= NN ? pfa_base - NN : pfa_base;
-            // t(e) = r + ((q + e) mod P) SE with base = q SE + r: valid iff
-            // (q + e) mod P < m = ceil((W - r) / SE); P == 32, so the valid-e mask
-            // is the low-m-bits mask rotated right by q
-            static_assert(!F::PFA || P == 32, "PFA lag mask assumes a 32-point last stage");
-            const uint32_t q = pfa_base / SE, r = pfa_base - q * SE;
-            const uint32_t m = W > r ? min(32u, (W - r + SE - 1) / SE) : 0u;
-            const uint32_t lowm = m >= 32u ? 0xffffffffu : (1u << m) - 1u;
-            pfa_mask = __funnelshift_r(lowm, lowm, q);
+            uint32_t base = NBB * ta + uint32_t(PA) * (tb1 + uint32_t(QA) * uint32_t(c));
+            base = base >= NN ? base - NN : base;
+            const uint32_t q = base / SE;
+            pfa_base = base - q * SE;   // r: the lag of slot 0
+            pfa_m = W > pfa_base ? min(uint32_t(P), (W - pfa_base + SE - 1) / SE) : 0u;
+            // w_1024^{a (c - 32 q)}: base twiddle and the 8j anchors
+            const float2 rq = anc[4 * Q + (q & 31u)];   // w_32^{-q}
+            const float2 t1 = cmul(anc[c], rq);
+            float2 t = t1;
+#pragma unroll
+            for (int a = 1; a < P; ++a) {
+                if (a % 8 == 0) {
+                    const float2 x = anc[(a / 8) * Q + c];
+                    const uint32_t k = (uint32_t(4 - (a / 8)) * q) & 3u;   // i^{-(a/8) q} = i^k
+                    t = k == 0 ? x : k == 1 ? make_float2(-x.y, x.x) : k == 2 ? make_float2(-x.x, -x.y)
+                                                                           : make_float2(x.y, -x.x);
+                } else if (a > 1) {
+                    t = cmul(t, t1);
+                }
+                w[a] = cmul(w[a], t);
+            }
+            dft<P, +1>(w);
             if (S.write_xc) {
 #pragma unroll
                 for (int e = 0; e < P; ++e) {
-                    if ((pfa_mask >> e) & 1u) {
-                        uint32_t t = pfa_base + uint32_t(e) * SE;
-                        t = t >= NN ? t - NN : t;
-                        if (po.xc_a) po.xc_a[t] = w[e].x * S.inv_n;
-                        if (po.xc_b) po.xc_b[t] = w[e].y * S.inv_n;
+                    if (uint32_t(e) < pfa_m) {
+                        const uint32_t tt = pfa_base + uint32_t(e) * SE;
+                        if (po.xc_a) po.xc_a[tt] = w[e].x * S.inv_n;
+                        if (po.xc_b) po.xc_b[tt] = w[e].y * S.inv_n;
+                    }
+                }
+            } else if (W >= uint32_t(P - 4) * SE) {
+                // every lane's m >= P - 4 (r < SE): the first P - 4 slots unmasked,
+                // three-input maxima
+#pragma unroll
+                for (int e = 0; e < P - 4; e += 2) {
+                    best_a = fmax3_abs(best_a, w[e].x, w[e + 1].x);
+                    best_b = fmax3_abs(best_b, w[e].y, w[e + 1].y);
+                }
+#pragma unroll
+                for (int e = P - 4; e < P; ++e) {
+                    if (uint32_t(e) < pfa_m) {
+                        best_a = fmaxf(best_a, fabsf(w[e].x));
+                        best_b = fmaxf(best_b, fabsf(w[e].y));
                     }
                 }
             } else {
 #pragma unroll
                 for (int e = 0; e < P; ++e) {
-                    if ((pfa_mask >> e) & 1u) {
+                    if (uint32_t(e) < pfa_m) {
                         best_a = fmaxf(best_a, fabsf(w[e].x));
                         best_b = fmaxf(best_b, fabsf(w[e].y));
                     }
                 }
             }
-        } else
+        } else {
+            apply_step2_twiddles_anc<P, Q>(w, anc, c);
+            dft<P, +1>(w);
+        }
         // valid lags t = t2 + N2*(c + Q*e) < W form a prefix e < e_lim
-        if (t2 < N2 && uint32_t(t2) < W) {
+        if (!F::PFA && t2 < N2 && uint32_t(t2) < W) {
             const int t1max = int((W - 1u - uint32_t(t2)) / uint32_t(N2));
             e_lim = t1max >= c ? (t1max - c) / Q + 1 : 0;
             e_lim = e_lim < P ? e_lim : P;
         }
-        if (S.write_xc) {
+        if (F::PFA) {
+        } else if (S.write_xc) {
 #pragma unroll
             for (int e = 0; e < P; ++e) {
                 if (e < e_lim) {
@@ -494,20 +536,20 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
         const bool need_a = __any_sync(0xffffffffu, best_a >= 0.f && best_a >= cur_a);
         const bool need_b = __any_sync(0xffffffffu, best_b >= 0.f && po.key_b != nullptr && best_b >= cur_b);
         if (F::PFA && (need_a || need_b)) {   // warp-uniform
-            // smallest lag among this lane's maxima (lags are not monotone in e)
+            // smallest lag among this lane's maxima (lags rise with the slot)
             constexpr uint32_t NN = uint32_t(F::LA) * uint32_t(F::LB), SE = NN / P;
             uint32_t ta = 0xffffffffu, tb = 0xffffffffu;
             if (c < Q) {
 #pragma unroll
-                for (int e = 0; e < P; ++e) {
-                    if ((pfa_mask >> e) & 1u) {
-                        uint32_t t = pfa_base + uint32_t(e) * SE;
-                        t = t >= NN ? t - NN : t;
-                        if (fabsf(w[e].x) == best_a) ta = min(ta, t);
-                        if (fabsf(w[e].y) == best_b) tb = min(tb, t);
+                for (int e = P - 1; e >= 0; --e) {
+                    if (uint32_t(e) < pfa_m) {
+                        const uint32_t t = pfa_base + uint32_t(e) * SE;
+                        if (fabsf(w[e].x) == best_a) ta = t;
+                        if (fabsf(w[e].y) == best_b) tb = t;
                     }
                 }
             }
+            (void)NN;
             unsigned long long ka = need_a && ta != 0xffffffffu ? peak_key(best_a, po.lag0 + ta) : 0ull;
             unsigned long long kb = need_b && tb != 0xffffffffu ? peak_key(best_b, po.lag0 + tb) : 0ull;
 #pragma unroll
@@ -601,10 +643,17 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
         D.groups = reinterpret_cast<const CorrGroup<kGroup>*>(dsm);
         D.outs = reinterpret_cast<const CorrPairOut*>(dsm + nb_g);
     }
-    if (TYPE == 1)
+    if (TYPE == 1) {
         fill_twiddle_anchors<PB, QB>(anc, S.twB, threadIdx.x, F::NT);
-    else if (!F::PFA)
+        if (F::PFA && threadIdx.x < 32) {
+            // w_32^{-q}, q < 32: the rotation of the PFA epilogue's outputs
+            double sn, cs;
+            sincospi(double(threadIdx.x) / 16.0, &sn, &cs);
+            anc[4 * QB + threadIdx.x] = make_float2(float(cs), float(-sn));
+        }
+    } else if (!F::PFA) {
         fill_twiddle_anchors<PA, QA>(anc, S.twA, threadIdx.x, F::NT);
+    }
     __syncthreads();
     uint32_t phases = 0u;   // bit s: parity of slot s's mbarrier
     Ticket k = ticket_at(i0, den);
