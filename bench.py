@@ -351,43 +351,38 @@ def correctness_gate(recs, inj, code0, n_codes, ref_recs, bits, iq):
     return gate, problems
 
 
-def run_tracking(args):
+def tracking_probe(ctx, cfg, bits, iq, iq_dev, inj, steps, warmup, with_cpu=True, batches=(1, 8, 64, 512)):
     """BASELINE configs[3]: tracking tasks (proj/src/scheduler.cpp:89-113,
     recording.cpp:360-378) -- 12 ms windows [toa - 2 ms, toa + 10 ms) at
-    8 Ms/s, one code each, in latency-bound batches of 1, 8, 64, 512 tasks
-    through tdg_track_device (stream resident on the device, i.e. the
-    device-side CircularBuffer; Detection records copied back to the host
-    inside the timed call).  Reports tasks/s and per-batch latency
-    percentiles (host wall clock around each synchronous call)."""
+    8 Ms/s, one code each, in latency-bound batches through tdg_track_device
+    (stream resident on the device, i.e. the device-side CircularBuffer;
+    Detection records copied back to the host inside the timed call).
+    Returns per-batch tasks/s and latency percentiles (host wall clock around
+    each synchronous call), the reference's CPU figure beside them and the
+    parity of 32 tasks against the reference."""
     import ctypes
 
     import torch
-    rank, local, world = dist_env()
-    torch.cuda.set_device(local)
     from paper_2005_10445_b200 import capi
-    from paper_2005_10445_b200._abi import DETECTION_DTYPE, TRACK_TASK_DTYPE, demod_config
+    from paper_2005_10445_b200._abi import DETECTION_DTYPE, TRACK_TASK_DTYPE
     lib = capi.lib()
-    cfg = demod_config()
-    bits, iq, inj, _ = make_inputs(rank, world)
     TW, PRE = 96000, 16000
     n = iq.size // 2
-    ctx = capi.Context(local)
     cs = capi.CodeSet.prepare(ctx, cfg, TW, bits)
-    iq_dev = torch.from_numpy(iq).to(f"cuda:{local}")
     rng = np.random.default_rng(5)
     # predicted arrivals: the injected packets (hits) and random times for
     # the other codes (misses), as the scheduler issues them
     pool = [(int(round(t * FS)) - PRE, ci) for ci, t, _, _ in inj]
     while len(pool) < 4096:
-        pool.append((int(rng.integers(0, n - TW)), int(rng.integers(0, N_CODES))))
+        pool.append((int(rng.integers(0, n - TW)), int(rng.integers(0, len(bits)))))
     pool = [(max(0, min(s0, n - TW)), c) for s0, c in pool]
     res = {}
-    for B in (1, 8, 64, 512):
+    for B in batches:
         tasks = np.zeros(B, dtype=TRACK_TASK_DTYPE)
         out = np.zeros(B, dtype=DETECTION_DTYPE)
         lat = []
-        reps = max(args.steps, 20) if B < 512 else max(args.steps, 10)
-        for r in range(args.warmup + reps):
+        reps = max(steps, 20) if B < 512 else max(steps, 10)
+        for r in range(warmup + reps):
             sel = [pool[(r * B + i) % len(pool)] for i in range(B)]
             tasks["start"] = [x[0] for x in sel]
             tasks["code_index"] = [x[1] for x in sel]
@@ -396,7 +391,7 @@ def run_tracking(args):
             capi._check(lib.tdg_track_device(ctx.handle, ctypes.byref(cfg), ctypes.c_void_p(iq_dev.data_ptr()), n, 0,
                                              capi._ptr(tasks), B, cs._h, 0.25, capi._ptr(out)))
             dt = time.perf_counter() - t0
-            if r >= args.warmup:
+            if r >= warmup:
                 lat.append(dt)
         lat = np.array(lat)
         res[str(B)] = {"tasks_per_s": B / float(np.mean(lat)), "p50_ms": float(np.percentile(lat, 50) * 1e3),
@@ -410,7 +405,7 @@ def run_tracking(args):
     cpu, parity = None, None
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import refpy
-    if refpy.available() and not args.no_cpu_baseline:
+    if refpy.available() and with_cpu:
         sel = pool[:32]
         st = np.array([x[0] for x in sel], np.int64)
         co = np.array([x[1] for x in sel], np.uint64)
@@ -434,11 +429,29 @@ def run_tracking(args):
         if bad:
             sys.stderr.write(json.dumps({"error": "tracking parity failed", "bad": [str(b) for b in bad[:10]]}) + "\n")
             sys.exit(3)
+    corr_len = cs.info(0)["corr_len"]
+    cs.close()
+    return res, cpu, parity, corr_len
+
+
+def run_tracking(args):
+    """BASELINE configs[3] as its own line (see tracking_probe)."""
+    import torch
+    rank, local, world = dist_env()
+    torch.cuda.set_device(local)
+    from paper_2005_10445_b200 import capi
+    from paper_2005_10445_b200._abi import demod_config
+    cfg = demod_config()
+    bits, iq, inj, _ = make_inputs(rank, world)
+    ctx = capi.Context(local)
+    iq_dev = torch.from_numpy(iq).to(f"cuda:{local}")
+    res, cpu, parity, corr_len = tracking_probe(ctx, cfg, bits, iq, iq_dev, inj, args.steps, args.warmup,
+                                                with_cpu=not args.no_cpu_baseline)
     line = {"metric": "tracking tasks/sec", "value": res["512"]["tasks_per_s"], "unit": "tasks/s", "n_gpus": 1,
             "higher_is_better": True, "dtype": "f32", "data": "synthetic (cfg2 scene; 16 injected packets tracked, "
             "other tasks are misses at random predicted times)",
             "config": {"workload": "cfg4: tracking windows W=96000 (2 ms pre + 10 ms post at 8 Ms/s), one code per "
-                                   "task, batches of 1/8/64/512", "corr_len_b200": cs.info(0)["corr_len"]},
+                                   "task, batches of 1/8/64/512", "corr_len_b200": corr_len},
             "batches": res, "cpu_baseline": cpu, "parity": parity}
     print(json.dumps(line))
 
@@ -607,6 +620,16 @@ def main():
     wall_ms = max_over_ranks((time.perf_counter() - t0) * 1e3 / args.steps)
     e2e = n_units * world / (e2e_ms / 1e3)
 
+    # ---- per-kernel CUDA events (same steps, separate pass: recording an
+    # event pair around each of ~800 launches perturbs the step time) -------
+    ctx.kernel_time_reset()
+    ctx.set_option("time_kernels", 1)
+    for _ in range(args.steps):
+        step_device()
+    barrier()
+    kt = {k: ctx.kernel_time(k) for k in ("demod", "fwd_pass1", "fwd_pass2", "corr", "stats")}
+    ctx.set_option("time_kernels", 0)
+
     # ---- GPU code preparation (prepare_code for the whole
     # set -- synth_replica, demodulation, support/energy, forward transforms of
     # the code pairs), a fresh set of the same codes, outside the timed steps
@@ -624,15 +647,18 @@ def main():
                  "note": "wall clock of tdg_codeset_prepare (synchronous; fresh device buffers each time), "
                          "window_len %d, best of 3" % W}
 
-    # ---- per-kernel CUDA events (same steps, separate pass: recording an
-    # event pair around each of ~800 launches perturbs the step time) -------
-    ctx.kernel_time_reset()
-    ctx.set_option("time_kernels", 1)
-    for _ in range(args.steps):
-        step_device()
-    barrier()
-    kt = {k: ctx.kernel_time(k) for k in ("demod", "fwd_pass1", "fwd_pass2", "corr", "stats")}
-    ctx.set_option("time_kernels", 0)
+    # ---- tracking (BASELINE configs[3]) on the same box, so its latency and
+    # the reference's CPU figure beside it appear in the driver-visible line
+    # (outside every timed region of this line; single-rank runs only)
+    tracking = None
+    if world == 1 and args.workload == "search":
+        tres, tcpu, tpar, _ = tracking_probe(ctx, cfg, bits, iq, iq_dev, inj, args.steps, args.warmup,
+                                             with_cpu=not args.no_cpu_baseline)
+        tracking = {"workload": "cfg4: W=96000 windows, one code per task, tdg_track_device",
+                    "p50_ms": {k: round(v["p50_ms"], 4) for k, v in tres.items()},
+                    "p99_ms": {k: round(v["p99_ms"], 4) for k, v in tres.items()},
+                    "tasks_per_s": {k: round(v["tasks_per_s"], 1) for k, v in tres.items()},
+                    "cpu_baseline": tcpu, "parity": tpar}
 
     # ---- roofline of the dominant stage: the correlation engine -------------
     # (k_corr_pass pass A + pass B on overlapped streams, one per-step event
@@ -691,6 +717,7 @@ def main():
                         "overlapping the search of step k"},
         "gpu_launches": int(launches),
         "code_prep": code_prep,
+        "tracking": tracking,
         "roofline": dict(roof, **{
             "kernel": "correlation engine per step: k_corr_pass<27,32,32,32,0> (spectral product + first "
                       "inverse-FFT pass) and k_corr_pass<...,1> (second pass + argmax) in waves over 6 pass-A + 6 "
