@@ -135,6 +135,13 @@ __device__ __forceinline__ int tid_x() {
 // An item's coordinates: pass A (u, v) = (column pair cp, group), item
 // u * ngw + v; pass B (u, v) = (pair, M tile), item u * n_tiles + v.  A CTA
 // walks a contiguous item range, so they advance without divisions.
+// warp-wide max of a float (CREDUX.MAX.F32, sm_100a)
+__device__ __forceinline__ float warp_max_f32(float v) {
+    float d;
+    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(d) : "f"(v));
+    return d;
+}
+
 // max(m, |x|, |y|) as one FMNMX3 (three-input max with |.| operand modifiers)
 __device__ __forceinline__ float fmax3_abs(float m, float x, float y) {
     float d;
@@ -520,74 +527,49 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
         }
     }
     if (!S.write_xc) {
-        // first-index argmax.  Warp maxima of |Re|, |Im| first; only warps
-        // whose maximum can still win against the pair's best so far (read at
-        // item start -- an older value only makes more warps search) locate
-        // their first index and merge packed keys (magnitude, then smallest
-        // index: exact first-index ties) with atomicMax.
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            best_a = fmaxf(best_a, __shfl_xor_sync(0xffffffffu, best_a, o));
-            best_b = fmaxf(best_b, __shfl_xor_sync(0xffffffffu, best_b, o));
-        }
+        // first-index argmax.  Warp maxima of |Re|, |Im| first (one CREDUX
+        // each); only warps whose maximum can still win against the pair's
+        // best so far (read at item start -- an older value only makes more
+        // warps search) locate the smallest lag holding it (per lane, then one
+        // CREDUX.MIN) and merge packed keys (magnitude, then smallest lag:
+        // exact first-index ties) with atomicMax.
+        best_a = warp_max_f32(best_a);
+        best_b = warp_max_f32(best_b);
         // each lane read the pair's best on its own, so another CTA's atomicMax
-        // can land between lanes: vote, so the branch below (full-warp
-        // shuffles) is taken by every lane or none
+        // can land between lanes: vote, so the branch below (warp-wide
+        // reductions) is taken by every lane or none
         const bool need_a = __any_sync(0xffffffffu, best_a >= 0.f && best_a >= cur_a);
         const bool need_b = __any_sync(0xffffffffu, best_b >= 0.f && po.key_b != nullptr && best_b >= cur_b);
-        if (F::PFA && (need_a || need_b)) {   // warp-uniform
-            // smallest lag among this lane's maxima (lags rise with the slot)
-            constexpr uint32_t NN = uint32_t(F::LA) * uint32_t(F::LB), SE = NN / P;
+        if (need_a || need_b) {   // warp-uniform
             uint32_t ta = 0xffffffffu, tb = 0xffffffffu;
             if (c < Q) {
+                if (F::PFA) {
+                    // lags rise with the slot
+                    constexpr uint32_t NN = uint32_t(F::LA) * uint32_t(F::LB), SE = NN / P;
 #pragma unroll
-                for (int e = P - 1; e >= 0; --e) {
-                    if (uint32_t(e) < pfa_m) {
-                        const uint32_t t = pfa_base + uint32_t(e) * SE;
-                        if (fabsf(w[e].x) == best_a) ta = t;
-                        if (fabsf(w[e].y) == best_b) tb = t;
+                    for (int e = P - 1; e >= 0; --e) {
+                        if (uint32_t(e) < pfa_m) {
+                            const uint32_t t = pfa_base + uint32_t(e) * SE;
+                            if (fabsf(w[e].x) == best_a) ta = t;
+                            if (fabsf(w[e].y) == best_b) tb = t;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int e = P - 1; e >= 0; --e) {
+                        if (e < e_lim) {
+                            const uint32_t t = uint32_t(t2) + uint32_t(N2) * uint32_t(c + Q * e);
+                            if (fabsf(w[e].x) == best_a) ta = t;
+                            if (fabsf(w[e].y) == best_b) tb = t;
+                        }
                     }
                 }
             }
-            (void)NN;
-            unsigned long long ka = need_a && ta != 0xffffffffu ? peak_key(best_a, po.lag0 + ta) : 0ull;
-            unsigned long long kb = need_b && tb != 0xffffffffu ? peak_key(best_b, po.lag0 + tb) : 0ull;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const unsigned long long xa = __shfl_xor_sync(0xffffffffu, ka, o);
-                const unsigned long long xb = __shfl_xor_sync(0xffffffffu, kb, o);
-                ka = xa > ka ? xa : ka;
-                kb = xb > kb ? xb : kb;
-            }
+            ta = __reduce_min_sync(0xffffffffu, ta);
+            tb = __reduce_min_sync(0xffffffffu, tb);
             if ((tid & 31) == 0) {
-                if (ka) atomicMax(po.key_a, ka);
-                if (kb) atomicMax(po.key_b, kb);
-            }
-        } else if (need_a || need_b) {   // warp-uniform
-            int ea = P, eb = P;
-            if (c < Q) {
-#pragma unroll
-                for (int e = P - 1; e >= 0; --e) {
-                    if (e < e_lim) {
-                        if (fabsf(w[e].x) == best_a) ea = e;
-                        if (fabsf(w[e].y) == best_b) eb = e;
-                    }
-                }
-            }
-            unsigned long long ka = need_a && ea < P
-                ? peak_key(best_a, po.lag0 + uint32_t(t2) + uint32_t(N2) * uint32_t(c + Q * ea)) : 0ull;
-            unsigned long long kb = need_b && eb < P
-                ? peak_key(best_b, po.lag0 + uint32_t(t2) + uint32_t(N2) * uint32_t(c + Q * eb)) : 0ull;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const unsigned long long xa = __shfl_xor_sync(0xffffffffu, ka, o);
-                const unsigned long long xb = __shfl_xor_sync(0xffffffffu, kb, o);
-                ka = xa > ka ? xa : ka;
-                kb = xb > kb ? xb : kb;
-            }
-            if ((tid & 31) == 0) {
-                if (ka) atomicMax(po.key_a, ka);
-                if (kb) atomicMax(po.key_b, kb);
+                if (need_a && ta != 0xffffffffu) atomicMax(po.key_a, peak_key(best_a, po.lag0 + ta));
+                if (need_b && tb != 0xffffffffu) atomicMax(po.key_b, peak_key(best_b, po.lag0 + tb));
             }
         }
     }
