@@ -469,11 +469,16 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
             } else if (W >= uint32_t(P - 4) * SE) {
                 // every lane's m >= P - 4 (r < SE): the first P - 4 slots unmasked,
                 // three-input maxima
+                // four independent FMNMX3 chains per component (short dependency
+                // chains: the epilogue is latency-, not issue-bound)
+                float ma[4] = {best_a, best_a, best_a, best_a}, mb[4] = {best_b, best_b, best_b, best_b};
 #pragma unroll
                 for (int e = 0; e < P - 4; e += 2) {
-                    best_a = fmax3_abs(best_a, w[e].x, w[e + 1].x);
-                    best_b = fmax3_abs(best_b, w[e].y, w[e + 1].y);
+                    ma[(e / 2) & 3] = fmax3_abs(ma[(e / 2) & 3], w[e].x, w[e + 1].x);
+                    mb[(e / 2) & 3] = fmax3_abs(mb[(e / 2) & 3], w[e].y, w[e + 1].y);
                 }
+                best_a = fmaxf(fmaxf(ma[0], ma[1]), fmaxf(ma[2], ma[3]));
+                best_b = fmaxf(fmaxf(mb[0], mb[1]), fmaxf(mb[2], mb[3]));
 #pragma unroll
                 for (int e = P - 4; e < P; ++e) {
                     if (uint32_t(e) < pfa_m) {
