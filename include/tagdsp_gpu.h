@@ -246,6 +246,11 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value);
  * "stats".  Synchronises the context stream. */
 int tdg_kernel_time(tdg_ctx* ctx, const char* name, uint64_t* count, double* total_ms);
 int tdg_kernel_time_reset(tdg_ctx* ctx);
+/* Diagnostics (option "cta_trace" = capacity > 0): the correlation-pass CTAs
+ * recorded since the last call, 3 words each {smid << 8 | pass (0 = A, 1 = B),
+ * globaltimer ns at CTA start, at CTA exit}; *n = records (all of them, even
+ * beyond cap); the record count is reset.  Synchronises the device. */
+int tdg_cta_trace(tdg_ctx* ctx, uint64_t* out, uint64_t cap, uint64_t* n);
 /* FP32 issue-rate probe (bench.py's roofline denominator): TFLOP/s of scalar
  * FFMA and of packed FFMA2 on `device` at its current clock. */
 int tdg_fp32_peak(int device, double* ffma_tflops, double* ffma2_tflops);

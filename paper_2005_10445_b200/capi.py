@@ -94,6 +94,7 @@ _PROTOS = {
     "tdg_set_option": (ctypes.c_int, [_P, ctypes.c_char_p, _I64]),
     "tdg_kernel_time": (ctypes.c_int, [_P, ctypes.c_char_p, ctypes.POINTER(_U64), ctypes.POINTER(ctypes.c_double)]),
     "tdg_kernel_time_reset": (ctypes.c_int, [_P]),
+    "tdg_cta_trace": (ctypes.c_int, [_P, _P, _U64, ctypes.POINTER(_U64)]),
     "tdg_fft": (ctypes.c_int, [_P, _P, _P, _U64, ctypes.c_int]),
     "tdg_convert": (ctypes.c_int, [_P, _P, _U64, _P]),
     "tdg_mix": (ctypes.c_int, [_P, _P, _U64, ctypes.c_double, _I64, ctypes.c_double]),

@@ -111,6 +111,9 @@ struct CorrSched {                     // one wave
     int ngw, wave_pairs, n_tiles, nA, nB, N1, N2;
     int write_xc;                      // 1: full xc rows (batch_xcorr), 0: argmax keys
     int discard;                       // 1: drop consumed M tiles from L2 (no write-back)
+    unsigned long long* trace;         // diagnostics (option "cta_trace"): per CTA {smid|type, t0, t1}
+    unsigned int* trace_n;
+    unsigned int trace_cap;
     uint32_t W;                        // window length (lag limits are per pair: CorrPairOut)
     float inv_n;
 };
@@ -588,6 +591,8 @@ template <int PA, int QA, int PB, int QB, int TYPE>
 __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_constant__ CorrSched S) {
     using F = Fused<PA, QA, PB, QB>;
     extern __shared__ __align__(128) unsigned char smraw[];
+    unsigned long long trace_t0 = 0;
+    if (S.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trace_t0));
     uint64_t* bar = reinterpret_cast<uint64_t*>(smraw);   // [0..1]: slot full
     float2* slots = reinterpret_cast<float2*>(smraw + 128);
     float2* anc = slots + size_t(kSlots) * F::SLOT;      // step-2 twiddle anchors of this pass
@@ -694,6 +699,22 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
     // the stores' global writes are complete by the end of the grid (what
     // orders pass B after them), so only the reads are waited for here
     if (TYPE == 0 && lane == 0) bulk_wait_read_all();
+    if (S.trace) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t1, smid;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            unsigned int sm32;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm32));
+            smid = sm32;
+            const unsigned int i = atomicAdd(S.trace_n, 1u);
+            if (i < S.trace_cap) {
+                S.trace[3 * size_t(i)] = (smid << 8) | unsigned(TYPE);
+                S.trace[3 * size_t(i) + 1] = trace_t0;
+                S.trace[3 * size_t(i) + 2] = t1;
+            }
+        }
+    }
 }
 
 }  // namespace tdg

@@ -564,6 +564,10 @@ struct tdg_ctx {
     int64_t discard = 1;         // drop consumed M tiles from L2
     int64_t one_stream = 0;      // tuning: run pass B on the context stream too (no overlap)
     int64_t fwd_wave = 32;       // sequence pairs per forward-FFT wave
+    // diagnostics: option "cta_trace" = capacity; every correlation-pass CTA
+    // records {smid << 8 | pass, globaltimer at start, at exit} (tdg_cta_trace)
+    DevBuf trace;
+    uint32_t trace_cap = 0;
     // max CTAs per SM of pass A / pass B (0 = occupancy).  Pass B at 2 of its 3
     // leaves SM room for the next waves' pass A on the other streams (A/B: +0.8 %
     // device and e2e, burst and sustained)
@@ -1120,6 +1124,11 @@ void run_correlations(tdg_ctx* ctx, tdg_windows* w, const tdg_codeset* cs, const
     S.N2 = N2;
     S.write_xc = write_xc ? 1 : 0;
     S.discard = ctx->discard ? 1 : 0;
+    if (ctx->trace_cap && !tl_graph_mode) {
+        S.trace = reinterpret_cast<unsigned long long*>(ctx->trace.as<unsigned char>() + 16);
+        S.trace_n = ctx->trace.as<unsigned int>();
+        S.trace_cap = ctx->trace_cap;
+    }
     S.W = uint32_t(w->W);
     S.inv_n = 1.0f / float(N);
     auto* gd = ctx->pk->corr.at<tdg::CorrGroup<G>>(og);
@@ -1250,6 +1259,24 @@ int tdg_kernel_time(tdg_ctx* ctx, const char* name, uint64_t* count, double* tot
     });
 }
 
+int tdg_cta_trace(tdg_ctx* ctx, uint64_t* out, uint64_t cap, uint64_t* n) {
+    return guard([&] {
+        CK(cudaSetDevice(ctx->device));
+        CK(cudaStreamSynchronize(ctx->stream));
+        CK(cudaDeviceSynchronize());
+        uint32_t cnt = 0;
+        if (ctx->trace_cap) {
+            CK(cudaMemcpy(&cnt, ctx->trace.p, sizeof(cnt), cudaMemcpyDeviceToHost));
+            cnt = std::min(cnt, ctx->trace_cap);
+            const uint64_t m = std::min<uint64_t>(cnt, cap);
+            if (out && m)
+                CK(cudaMemcpy(out, ctx->trace.as<unsigned char>() + 16, m * 24, cudaMemcpyDeviceToHost));
+            CK(cudaMemset(ctx->trace.p, 0, 16));
+        }
+        if (n) *n = cnt;
+    });
+}
+
 int tdg_kernel_time_reset(tdg_ctx* ctx) {
     return guard([&] {
         ctx->collect();
@@ -1287,6 +1314,13 @@ int tdg_set_option(tdg_ctx* ctx, const char* key, int64_t value) {
             ctx->track_graphs_on = value != 0;
         else if (k == "fwd_wave")
             ctx->fwd_wave = value > 0 ? value : 32;
+        else if (k == "cta_trace") {
+            ctx->trace_cap = uint32_t(std::max<int64_t>(0, value));
+            if (ctx->trace_cap) {
+                ctx->trace.ensure(size_t(ctx->trace_cap) * 24 + 16);
+                CK(cudaMemsetAsync(ctx->trace.p, 0, size_t(ctx->trace_cap) * 24 + 16, ctx->stream));
+            }
+        }
         else if (k == "detect_timings")
             ctx->detect_timings = value != 0;
         else
