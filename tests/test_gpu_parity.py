@@ -514,3 +514,31 @@ def test_window_lengths_beyond_the_menu(gpu_ctx, ref, W):
     for i in range(len(bits)):
         e = cs.info(i)["energy"]
         assert np.abs(got[i] - xc[i]).max() <= 2e-5 * e, i
+
+
+def test_cta_trace_diagnostics(gpu_ctx, ref):
+    """Option cta_trace + tdg_cta_trace: every correlation-pass CTA of a
+    detect records its SM and start/exit times (tools/cta_trace.py)."""
+    import ctypes
+
+    from paper_2005_10445_b200 import capi
+    W = 2048
+    dcs = [ref.gaussian(8100 + i, 100) for i in range(6)]
+    d = ref.gaussian(8199, W)
+    cs = _cs_from(capi, gpu_ctx, dcs, W, ref)
+    w = capi.Windows(gpu_ctx, W)
+    w.set_du(0, d, d)
+    gpu_ctx.set_option("cta_trace", 4096)
+    try:
+        capi.detect(gpu_ctx, w, cs)
+        buf = np.zeros(3 * 4096, dtype=np.uint64)
+        n = ctypes.c_uint64()
+        capi._check(capi.lib().tdg_cta_trace(gpu_ctx.handle, capi._ptr(buf), 4096, ctypes.byref(n)))
+        rec = buf[:3 * n.value].reshape(-1, 3)
+        assert n.value > 0
+        assert set((rec[:, 0] & 255).tolist()) == {0, 1}          # both passes
+        assert (rec[:, 2] >= rec[:, 1]).all() and (rec[:, 1] > 0).all()
+        capi._check(capi.lib().tdg_cta_trace(gpu_ctx.handle, capi._ptr(buf), 4096, ctypes.byref(n)))
+        assert n.value == 0                                         # read resets the count
+    finally:
+        gpu_ctx.set_option("cta_trace", 0)
