@@ -382,9 +382,9 @@ __device__ __forceinline__ void store_passA_role(const CorrSched& S, const Desc&
 // Epilogue: first-index argmax of |Re|, |Im| over lags t < W (find_peak,
 // proj/src/detector.cpp:122-134) merged with atomicMax on packed keys, or
 // the full xc rows (batch_xcorr diagnostics).
-template <int PA, int QA, int PB, int QB>
+template <int PA, int QA, int PB, int QB, class Pre>
 __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, const Ticket& k, float2* sl,
-                                           const float2* anc) {
+                                           const float2* anc, Pre&& pre) {
     using F = Fused<PA, QA, PB, QB>;
     constexpr int P = PB, Q = QB, ROW = F::ROWB, TB = kTileB;
     const CorrPairOut& po = D.outs[k.u];
@@ -409,6 +409,9 @@ __device__ __forceinline__ void item_passB(const CorrSched& S, const Desc& D, co
         dft<Q, +1>(v);
     }
     __syncthreads();   // in place: every input read before any transposed write
+    // every warp is past the previous item, so the other slot is free: the
+    // next tile's bulk copy (no end-of-item barrier needed)
+    pre();
     if (act1) {
 #pragma unroll
         for (int c = 0; c < Q; ++c) tr[a1 * ROW + c * TB + t2l1] = v[c];
@@ -665,9 +668,9 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
             if (TYPE == 1 && threadIdx.x == 0 && !ticket_noop<TYPE>(D, kn))
                 issue_tile<PA, QA, PB, QB>(D, kn, slots + size_t(s ^ 1) * F::SLOT, &bar[s ^ 1]);
         };
-        if (TYPE == 1) prefetch();
         if (ticket_noop<TYPE>(D, k)) {
-            if (TYPE == 0) prefetch();
+            if (TYPE == 1) __syncthreads();   // every warp past the previous item
+            prefetch();
             k = kn;
             continue;
         }
@@ -689,9 +692,11 @@ __global__ void __launch_bounds__(128, TDG_CORR_MINB) k_corr_pass(const __grid_c
             if (S.discard)
                 for (uintptr_t a = lo + uintptr_t(threadIdx.x) * 128; a < hi; a += uintptr_t(F::NT) * 128)
                     discard_l2(reinterpret_cast<const void*>(a));
-            item_passB<PA, QA, PB, QB>(S, D, k, sl, anc);
+            item_passB<PA, QA, PB, QB>(S, D, k, sl, anc, prefetch);
         }
-        __syncthreads();   // slot s consumed (pass A: its staged columns complete)
+        // pass A: slot s consumed, its staged columns complete (pass B needs no
+        // end-of-item barrier: its next bulk copy waits for the in-item one)
+        if (TYPE == 0) __syncthreads();
         if (TYPE == 0 && lane == 0) store_passA_role<PA, QA, PB, QB>(S, D, k, sl, warp);
         k = kn;
     }
