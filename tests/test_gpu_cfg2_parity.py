@@ -134,6 +134,7 @@ def test_cfg2_sweep_against_reference(gpu_ctx, ref, scene):
     assert found >= 12
     assert not allbad, allbad[:20]
     assert rep.records == len(CHECK_WINDOWS) * BINS.size * len(bits)
+    _assert_plain_tolerance(rep)
 
 
 def test_roster_1024_against_reference(gpu_ctx, ref, scene):
@@ -160,3 +161,15 @@ def test_roster_1024_against_reference(gpu_ctx, ref, scene):
     _write_report([rep], "")
     assert not bad, bad[:20]
     assert rep.records == 1024
+    _assert_plain_tolerance(rep)
+
+
+def _assert_plain_tolerance(rep):
+    """SURVEY 8(c)'s plain bounds hold outright on every accepted record
+    (the conditioning-aware bound of tests/parity.py is only needed for weak,
+    rejected peaks): sub-sample offset / ToA within 1e-4 samples, peak value,
+    w_c, q, p_c and score within 1e-4 relative."""
+    m = rep.max_rel_accepted
+    assert m["subsample_offset"] <= 1e-4 and m["toa_samples"] <= 1e-4, m
+    for f in ("peak_value", "w_c", "q", "p_c", "score"):
+        assert m[f] <= 1e-4, (f, m[f])
